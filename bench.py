@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the PQR hot path (BASELINE.json metric:
+"PQR effective HBM GB/s (fraction of roofline) at 1/2/4/8 B200, fp64").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload weak|single|deflation|tiny]
+                  [--variant cholqr2|tsqr|both] [--impl pqr|reference]
+
+One step = one pqr_project_normalize call per selected variant (PQR_NO_APPEND, so the
+basis and all inputs are identical every step) over the workload's synthetic block.
+Default workload = configs[4] ("weak": 2^25 rows per GPU, k=128, s=8), the config the
+metric is quoted on at 1/2/4/8 GPUs; per-GPU work is fixed, so scaling is "weak".
+
+value = whole-job effective GB/s = sum over ranks of the MANDATORY bytes of a call
+(Q and X read once, U written once: 8 n_local (k + 2s)) x calls / max-over-ranks time.
+--impl reference times the CPU oracle (oracle/, plain C fp64 Householder) on a bounded
+row sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 2204133930
+WORKLOADS = {
+    "tiny": dict(n=10_000, k=32, s=4, cfg_index=0),
+    "single": dict(n=2 ** 24, k=64, s=8, cfg_index=1),
+    "deflation": dict(n=2 ** 22, k=96, s=16, cfg_index=3),
+    "weak": dict(n=2 ** 25, k=128, s=8, cfg_index=4),
+}
+METRIC = "PQR effective HBM GB/s (fraction of roofline) at 1/2/4/8 B200, fp64"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def mandatory_bytes(n, k, s):
+    return 8.0 * n * (k + 2 * s)
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (nvml) — runs during the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.hd = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hd, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.hd, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    getattr(self.nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+                r = fn(self.hd)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, bounded sample)
+# --------------------------------------------------------------------------
+def oracle_sample(w, target_s=15.0, max_rows=None):
+    """Time the oracle (as it stands) on a row sample of the workload; returns (GB/s, info)."""
+    import numpy as np
+
+    import oracle
+    from paper_2204_13393_b200 import inputs
+
+    k, s = w["k"], w["s"]
+    n_full = w["n"]
+    rows = min(n_full, 2 ** 14)
+    Q = inputs.orthonormal(SEED + 11, rows, k)
+    X = inputs.gaussian(SEED + 12, rows, s)
+    t0 = time.perf_counter()
+    oracle.householder_pqr(Q, X)
+    dt = time.perf_counter() - t0
+    # scale the sample to ~target_s seconds (the oracle is O(n) per call)
+    rows2 = int(min(n_full, max(rows, rows * target_s / max(dt, 1e-3) * 0.8)))
+    if max_rows:
+        rows2 = min(rows2, max_rows)
+    if rows2 > rows:
+        rows = rows2
+        Q = inputs.orthonormal(SEED + 11, rows, k)
+        X = inputs.gaussian(SEED + 12, rows, s)
+        t0 = time.perf_counter()
+        oracle.householder_pqr(Q, X)
+        dt = time.perf_counter() - t0
+    gbs = mandatory_bytes(rows, k, s) / dt / 1e9
+    info = {"value": gbs, "unit": "GB/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"one Householder PQR of [Q X] with {rows} of the workload's {n_full} rows "
+                      f"(k={k}, s={s}), {dt:.2f} s; GB/s = 8*rows*(k+2s)/time"}
+    return gbs, info, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    w = WORKLOADS[args.workload]
+    _, info, dt1 = oracle_sample(w, target_s=min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    # the steps: repeat the same bounded sample
+    import numpy as np
+
+    import oracle
+    from paper_2204_13393_b200 import inputs
+
+    rows = int(info["sample"].split(" with ")[1].split(" of ")[0])
+    Q = inputs.orthonormal(SEED + 11, rows, w["k"])
+    X = inputs.gaussian(SEED + 12, rows, w["s"])
+    for _ in range(args.warmup):
+        oracle.householder_pqr(Q, X)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.householder_pqr(Q, X)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = mandatory_bytes(rows, w["k"], w["s"]) * args.steps / tot / 1e9
+    info["value"] = val
+    line = {"metric": METRIC, "value": val, "unit": "GB/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "n_local": w["n"], "k": w["k"], "s": w["s"],
+                       "sample_rows": rows, "parallelism": f"dp{world}"},
+            "cpu_baseline": info,
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="weak", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="cholqr2", choices=["cholqr2", "tsqr", "both"])
+    ap.add_argument("--impl", default="pqr", choices=["pqr", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "RANK" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_13393_b200 import inputs, pqr
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+    w = WORKLOADS[args.workload]
+    n, k, s = w["n"], w["k"], w["s"]
+    stream = torch.cuda.current_stream(device)
+
+    # ---- inputs (seeded, synthetic, on the device) ----
+    torch.cuda.synchronize()
+    if args.workload == "weak":
+        Q, X = inputs.device_weak_inputs(SEED + 4, n, k, s, device, rank=rank, world=world)
+    elif args.workload == "single":
+        Q, X = inputs.device_projected_inputs(SEED + 1, n, k, s, device)
+    elif args.workload == "deflation":
+        Q, X = inputs.device_deflation_inputs(SEED + 3, n, k, s, device)
+    else:
+        Qh, Xh = inputs.tiny_inputs(SEED, n, k, s)
+        Q = torch.from_numpy(np.ascontiguousarray(Qh.T)).to(device).t()
+        X = torch.from_numpy(np.ascontiguousarray(Xh.T)).to(device).t()
+    U = inputs.colmajor_empty(n, s, device)
+    Pm = inputs.colmajor_empty(k, s, device)
+    Nm = inputs.colmajor_empty(s, s, device)
+    torch.cuda.synchronize()
+
+    nccl_id = None
+    if world > 1:
+        obj = [pqr.pqr_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    variants = ["cholqr2", "tsqr"] if args.variant == "both" else [args.variant]
+    handles = {}
+    for v in variants:
+        handles[v] = pqr.PQR(n, k, s, Q, variant=v, stream=stream, rank=rank, nranks=world, nccl_id=nccl_id)
+    del Q
+    torch.cuda.empty_cache()
+
+    def step():
+        ts = []
+        for v in variants:
+            ts.append(handles[v].solve(X, U=U, P=Pm, N=Nm, flags=pqr.PQR_NO_APPEND))
+        return ts
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    for _ in range(args.warmup):
+        t_vals = step()
+    launches0 = sum(h.stats()["kernel_launches"] for h in handles.values())
+    for h in handles.values():
+        h.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            t_vals = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = sum(h.stats()["kernel_launches"] for h in handles.values()) - launches0
+    prof = {v: h.profile() for v, h in handles.items()}
+    tmax = torch.tensor([ms], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_max = float(tmax.item())
+    ms_step = ms_max / args.steps
+
+    mand = mandatory_bytes(n, k, s) * world * len(variants)  # per step, whole job
+    value = mand / (ms_step * 1e-3) / 1e9
+    hbm, peak_kind = peaks()
+
+    # ---- roofline of the dominant kernel (device events per launch, in the timed region) ----
+    kinds = {}
+    for v, p in prof.items():
+        for kind, d in p.items():
+            if d["launches"]:
+                kk = kinds.setdefault(kind, dict(ms=0.0, launches=0))
+                kk["ms"] += d["ms"]
+                kk["launches"] += d["launches"]
+    dom = max(kinds.items(), key=lambda kv: kv[1]["ms"])[0] if kinds else None
+    per_launch_bytes = {
+        "gram": 8.0 * n * (k + s),             # read Q, X (or Q, U1)
+        "update": 8.0 * n * (k + s) + 8.0 * n * s,  # read Q, X; write U
+        "tsqr_local": 8.0 * n * (k + s) + 8.0 * n * s,  # read Y (reflectors) and X, write new reflectors
+        "tsqr_apply": 8.0 * n * (k + s) + 8.0 * n * s,  # read Y, write U
+    }
+    roof = None
+    if dom in per_launch_bytes:
+        avg_ms = kinds[dom]["ms"] / kinds[dom]["launches"]
+        ach = per_launch_bytes[dom] / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tr = json.load(f)
+            traffic = tr.get(f"{args.workload}:{dom}")
+        except Exception:
+            traffic = None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes": per_launch_bytes[dom],
+                "avg_launch_ms": avg_ms}
+    share = {kd: (d["ms"] / (ms * 1.0)) for kd, d in kinds.items()}
+    t_roof = mandatory_bytes(n, k, s) / (hbm * 1e9) * 1e3 * len(variants)
+    frac_whole = t_roof / ms_step
+
+    # ---- e2e through the C-ABI with HOST buffers (pinned), copies inside the timed region ----
+    e2e = None
+    if args.e2e_steps > 0:
+        Xh = torch.empty((s, n), dtype=torch.float64, pin_memory=True).t()
+        Xh.copy_(X)
+        Uh = torch.empty((s, n), dtype=torch.float64, pin_memory=True).t()
+        Ph = torch.empty((s, k), dtype=torch.float64, pin_memory=True).t()
+        Nh = torch.empty((s, s), dtype=torch.float64, pin_memory=True).t()
+        for v in variants:
+            handles[v].solve(Xh, U=Uh, P=Ph, N=Nh, flags=pqr.PQR_NO_APPEND)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for v in variants:
+                handles[v].solve(Xh, U=Uh, P=Ph, N=Nh, flags=pqr.PQR_NO_APPEND)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=device, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e_step = float(dt.item()) / args.e2e_steps
+        e2e = {"value": mand / e2e_step / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 8 * n * s * len(variants),
+               "d2h_bytes_per_step": (8 * n * s + 8 * k * s + 8 * s * s) * len(variants),
+               "ms_per_step": e2e_step * 1e3}
+        del Xh, Uh
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            _, cpu, _ = oracle_sample(w, target_s=15.0)
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "error": str(e)}
+
+    for h in handles.values():
+        h.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "baseline_config": w["cfg_index"], "n_local": n, "k": k, "s": s,
+                       "global_rows": n * world, "variants": variants, "parallelism": f"dp{world}",
+                       "l2": "inputs exceed L2 (no flush needed)" if mandatory_bytes(n, k, s) > 2 * 126e6
+                       else "inputs fit in L2 (latency-bound config)",
+                       "t": t_vals},
+            "frac_of_roofline": frac_whole,
+            "roofline": roof,
+            "kernel_share": share,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,95 @@
+// common.cuh — device helpers shared by the libpqr kernels (sm_100a, fp64).
+//
+// The fp64 tensor-core instruction used throughout is the warp-level
+// mma.sync.aligned.m8n8k4.row.col.f64 (SASS: DMMA.8).  On B200 its measured
+// throughput equals the DFMA pipe's (37.0 vs 33.8 TFLOP/s fp64, see
+// profiles/r01_microbench.md) but it issues 1/256 of the instructions and keeps
+// the k-reduction inside the unit, which is what makes a one-warp-per-row-slab
+// tall-skinny Gram / update fit in the register file.
+//
+// Fragment layout (PTX ISA, m8n8k4 .f64; lane l, g = l>>2, q = l&3):
+//   A (8x4, row):  a0 = A[g][q]
+//   B (4x8, col):  b0 = B[q][g]
+//   C/D (8x8):     c0 = C[g][2q], c1 = C[g][2q+1]
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PQR_DEV __device__ __forceinline__
+
+namespace pqr {
+
+constexpr int kWarp = 32;
+
+PQR_DEV void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Streaming 16-byte load of two consecutive rows of one column (read-only path).
+PQR_DEV double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+PQR_DEV double2 ld2_stream(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
+
+PQR_DEV void st2(double* p, double x, double y) { *reinterpret_cast<double2*>(p) = make_double2(x, y); }
+
+// Column pointer of A = [Q X] (Q: columns 0..k-1, X: columns k..m-1); nullptr past m.
+PQR_DEV const double* col_ptr(const double* Q, int64_t ldq, const double* X, int64_t ldx, int k, int m, int j) {
+  if (j < k) return Q + (int64_t)j * ldq;
+  if (j < m) return X + (int64_t)(j - k) * ldx;
+  return nullptr;
+}
+
+// Guarded two-row load for ragged tails: rows r, r+1 of column c (nullptr -> 0).
+PQR_DEV double2 ld2_guard(const double* c, int64_t r, int64_t n) {
+  double2 v = make_double2(0.0, 0.0);
+  if (c) {
+    if (r < n) v.x = __ldg(c + r);
+    if (r + 1 < n) v.y = __ldg(c + r + 1);
+  }
+  return v;
+}
+
+}  // namespace pqr
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) + mbarrier pipeline primitives
+// ---------------------------------------------------------------------------
+namespace pqr {
+
+PQR_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+PQR_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+PQR_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+PQR_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+PQR_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+PQR_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+PQR_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, both addresses 16-B aligned)
+PQR_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace pqr

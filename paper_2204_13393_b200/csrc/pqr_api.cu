@@ -1,0 +1,840 @@
+// pqr_api.cu — the C-ABI of libpqr.so (include/pqr.h): handle, plans, the
+// CholQR2 (BCGS-PIP+) orchestration, the TSQR orchestration (tsqr_api.cuh),
+// NCCL plumbing and step-level entry points (include/pqr_steps.h).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <vector>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/pqr.h"
+#include "../../include/pqr_steps.h"
+#include "cholqr_kernels.cuh"
+#include "tsqr_kernels.cuh"
+#include "stream_kernels.cuh"
+
+using namespace pqr;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Ctx;
+int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k);
+int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, double* Ud, int64_t ldud,
+               bool append, int* t_host);
+int tsqr_apply(Ctx* h, const double* C, int ldc, int m, double* Y, int64_t ldy);
+void tsqr_free(Ctx* h);
+
+#define CUDA_TRY(x)                                   \
+  do {                                                \
+    cudaError_t e_ = (x);                             \
+    if (e_ != cudaSuccess) {                          \
+      fprintf(stderr, "[pqr] CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return PQR_ECUDA;                               \
+    }                                                 \
+  } while (0)
+#define NCCL_TRY(x)                                   \
+  do {                                                \
+    ncclResult_t r_ = (x);                            \
+    if (r_ != ncclSuccess) {                          \
+      fprintf(stderr, "[pqr] NCCL error %s at %s:%d\n", ncclGetErrorString(r_), __FILE__, __LINE__); \
+      return PQR_ENCCL;                               \
+    }                                                 \
+  } while (0)
+#define TRY(x)                   \
+  do {                           \
+    int rc_ = (x);               \
+    if (rc_ != PQR_OK) return rc_; \
+  } while (0)
+
+struct TsqrState;  // defined in tsqr_api.cuh
+
+struct Ctx {
+  pqr_config cfg{};
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  int k = 0;
+  int cap = 0;           // k_max + s_max
+  int64_t ld = 0;        // leading dimension of the explicit basis / staging buffers
+  double* basis = nullptr;  // CHOLQR2: explicit basis, n_local x cap
+  // CholQR2 workspaces
+  double* partials = nullptr;
+  int64_t partials_elems = 0;
+  unsigned int* ticket = nullptr;
+  double* Wloc = nullptr;   // m x s, compact (ld m) - this rank's Gram
+  double* Wall = nullptr;   // nranks x (m*s)
+  double *P1 = nullptr, *N1 = nullptr, *M1 = nullptr, *P2 = nullptr, *N2 = nullptr, *M2 = nullptr;
+  double *Pf = nullptr, *Nf = nullptr;
+  int* ints = nullptr;      // [0] t1 [1] t2 [2] tf [3] defl1 [4] defl2 [16..] piv1 [32..] piv2
+  int* h_ints = nullptr;    // pinned host mirror
+  double* stageX = nullptr;  // n x s_max staging for host X
+  double* stageU = nullptr;  // n x s_max staging for host U / internal U1
+  double* stageC = nullptr;  // cap x 16 staging for host C
+  ncclComm_t comm = nullptr;
+  pqr_stats st{};
+  TsqrState* ts = nullptr;
+  // profiling (pqr_profile_enable)
+  bool prof = false;
+  pqr_profile prof_tot{};
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { int kind; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+};
+
+struct ProfScope {
+  Ctx* h;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(Ctx* h_, int kind_) : h(h_), kind(kind_) {
+    if (!h->prof) return;
+    a = get_event();
+    cudaEventRecord(a, h->stream);
+  }
+  ~ProfScope() {
+    if (!h->prof || !a) return;
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, h->stream);
+    h->pending.push_back({kind, a, b});
+  }
+  cudaEvent_t get_event() {
+    if (!h->ev_pool.empty()) {
+      cudaEvent_t e = h->ev_pool.back();
+      h->ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+#define PQR_CAT2(a, b) a##b
+#define PQR_CAT(a, b) PQR_CAT2(a, b)
+#define PROF(h, kind) ProfScope PQR_CAT(prof_scope_, __LINE__)((h), (kind))
+
+void prof_collect(Ctx* h) {
+  for (auto& p : h->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      h->prof_tot.ms[p.kind] += ms;
+      h->prof_tot.launches[p.kind] += 1;
+    } else {
+      cudaGetLastError();
+    }
+    h->ev_pool.push_back(p.a);
+    h->ev_pool.push_back(p.b);
+  }
+  h->pending.clear();
+}
+
+bool is_host_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    return PQR_ENOMEM;
+  }
+  return PQR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel launchers (shared by the handle path and the step entry points)
+// ---------------------------------------------------------------------------
+int grid_cap(int sms) { return sms * 4; }
+
+struct GramPlan {
+  int G, MTW, NT, grid;
+  int64_t rows_per_cta;
+  size_t smem;
+};
+
+GramPlan plan_gram(int64_t n, int k, int s, int sms) {
+  GramPlan p{};
+  const int m = k + s;
+  const int MT = (m + 7) / 8;
+  p.NT = s > 8 ? 2 : 1;
+  p.G = 1;
+  while ((MT + p.G - 1) / p.G > 6) p.G *= 2;
+  p.MTW = (MT + p.G - 1) / p.G;
+  const int RW = 8 / p.G;
+  const int64_t min_rows = 8 * RW * 4;
+  int64_t target = (n + grid_cap(sms) - 1) / grid_cap(sms);
+  target = ((target + 7) / 8) * 8;
+  p.rows_per_cta = std::max<int64_t>(min_rows, target);
+  p.grid = (int)std::max<int64_t>(1, (n + p.rows_per_cta - 1) / p.rows_per_cta);
+  p.smem = (size_t)8 * p.MTW * p.NT * 64 * sizeof(double);
+  return p;
+}
+
+template <int MTW, int NT>
+cudaError_t launch_gram_t(const GramPlan& p, const GramArgs& a, bool vec, cudaStream_t st) {
+  if (vec) {
+    auto f = k_gram<MTW, NT, true>;
+    if (p.smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    f<<<p.grid, kThreads, p.smem, st>>>(a);
+  } else {
+    auto f = k_gram<MTW, NT, false>;
+    if (p.smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    f<<<p.grid, kThreads, p.smem, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t launch_gram_mtw(const GramPlan& p, const GramArgs& a, bool vec, cudaStream_t st) {
+  switch (p.MTW) {
+    case 1: return launch_gram_t<1, NT>(p, a, vec, st);
+    case 2: return launch_gram_t<2, NT>(p, a, vec, st);
+    case 3: return launch_gram_t<3, NT>(p, a, vec, st);
+    case 4: return launch_gram_t<4, NT>(p, a, vec, st);
+    case 5: return launch_gram_t<5, NT>(p, a, vec, st);
+    default: return launch_gram_t<6, NT>(p, a, vec, st);
+  }
+}
+
+constexpr int kSmemBudget = 225 * 1024;
+
+// ---- TMA tensor maps (driver entry point fetched through the runtime) ----
+typedef CUresult (*PFN_tmapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_tmapEncodeTiled tmap_encoder() {
+  static PFN_tmapEncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_tmapEncodeTiled>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+// rows x cols column-major fp64 (ld even, base 16-B aligned); box = kSlab rows x cols, no swizzle,
+// out-of-bounds rows read as zero.
+bool make_tmap(CUtensorMap* tm, const double* base, int64_t rows, int cols, int64_t ld) {
+  memset(tm, 0, sizeof(*tm));
+  if (cols <= 0) return true;
+  PFN_tmapEncodeTiled enc = tmap_encoder();
+  if (!enc || cols > 256) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)kSlab, (cuuint32_t)cols};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+StreamGeom stream_geom(int64_t n, int k, int sx, size_t extra_bytes, size_t min_stage_region) {
+  StreamGeom g{};
+  g.n = n; g.k = k; g.sx = sx;
+  g.k8 = (k + 7) / 8 * 8;
+  g.x8 = (sx + 7) / 8 * 8;
+  g.stage_dbl = (g.k8 + g.x8) * kSlab;
+  const size_t stage_bytes = (size_t)g.stage_dbl * sizeof(double);
+  // NS must be a multiple of the consumer-warp count: warp w owns stages w, w+8, ... so a
+  // warp never waits on a stage more than one mbarrier phase ahead (parity waits).
+  const size_t avail = kSmemBudget - 1024 - extra_bytes;
+  const int R = (int)std::max<size_t>(1, std::min<size_t>(3, avail / (kStreamConsumers * (stage_bytes + 16))));
+  g.NS = kStreamConsumers * R;
+  if ((size_t)g.NS * stage_bytes < min_stage_region) g.NS = 0;  // reduction would not fit: no TMA path
+  return g;
+}
+size_t stream_smem(const StreamGeom& g, size_t extra_bytes) {
+  return 1024 + (size_t)g.NS * g.stage_dbl * sizeof(double) + 2 * g.NS * sizeof(uint64_t) + extra_bytes;
+}
+
+template <int MTMAX, int NT>
+cudaError_t launch_gram_tma_t(int grid, size_t smem, const CUtensorMap& tq, const CUtensorMap& tx,
+                              const GramTmaArgs& a, cudaStream_t st) {
+  auto f = k_gram_tma<MTMAX, NT>;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  f<<<grid, kStreamThreads, smem, st>>>(tq, tx, a);
+  return cudaGetLastError();
+}
+
+// W (ld ldw) = [Q X]^T X over n rows.  partials must hold max(grid)*m*s doubles.
+int run_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double* X, int64_t ldx,
+             double* W, int ldw, double* partials, unsigned int* ticket, int sms, cudaStream_t st,
+             int64_t* launches) {
+  const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (ldx & 1) == 0 && aligned16(X);
+  const int m = k + s, MT = (m + 7) / 8;
+  const size_t red_bytes = (size_t)kStreamConsumers * MT * (s > 8 ? 2 : 1) * 64 * sizeof(double);
+  StreamGeom g = stream_geom(n, k, s, 0, red_bytes);
+  CUtensorMap tq, tx;
+  const bool tma = vec && MT <= 20 && g.NS >= 8 && stream_smem(g, 0) <= kSmemBudget + 2048 &&
+                   make_tmap(&tq, Q, n, k, ldq) && make_tmap(&tx, X, n, s, ldx);
+  cudaError_t e;
+  if (tma) {
+    GramTmaArgs a{};
+    a.g = g; a.partials = partials; a.W = W; a.ldw = ldw; a.ticket = ticket;
+    const size_t smem = stream_smem(g, 0);
+    const int grid = (int)std::min<int64_t>(sms, (n + kSlab - 1) / kSlab);
+    const int NT = s > 8 ? 2 : 1;
+    const int MB = MT <= 5 ? 5 : (MT <= 10 ? 10 : (MT <= 15 ? 15 : 20));
+    switch (MB * 10 + NT) {
+      case 51: e = launch_gram_tma_t<5, 1>(grid, smem, tq, tx, a, st); break;
+      case 52: e = launch_gram_tma_t<5, 2>(grid, smem, tq, tx, a, st); break;
+      case 101: e = launch_gram_tma_t<10, 1>(grid, smem, tq, tx, a, st); break;
+      case 102: e = launch_gram_tma_t<10, 2>(grid, smem, tq, tx, a, st); break;
+      case 151: e = launch_gram_tma_t<15, 1>(grid, smem, tq, tx, a, st); break;
+      case 152: e = launch_gram_tma_t<15, 2>(grid, smem, tq, tx, a, st); break;
+      case 201: e = launch_gram_tma_t<20, 1>(grid, smem, tq, tx, a, st); break;
+      default: e = launch_gram_tma_t<20, 2>(grid, smem, tq, tx, a, st); break;
+    }
+  } else {
+    const GramPlan p = plan_gram(n, k, s, sms);
+    GramArgs a{};
+    a.Q = Q; a.ldq = ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s;
+    a.G = p.G; a.rows_per_cta = p.rows_per_cta; a.partials = partials; a.W = W; a.ldw = ldw; a.ticket = ticket;
+    e = p.NT == 1 ? launch_gram_mtw<1>(p, a, vec, st) : launch_gram_mtw<2>(p, a, vec, st);
+  }
+  if (launches) ++*launches;
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[pqr] gram launch: %s\n", cudaGetErrorString(e));
+    return PQR_ECUDA;
+  }
+  return PQR_OK;
+}
+
+int64_t gram_partials_needed(int64_t n, int k, int s, int sms) {
+  const GramPlan p = plan_gram(n, k, s, sms);
+  return (int64_t)std::max(p.grid, sms) * (k + s) * s;
+}
+
+// U (cols < sout) = [Q X] M, optionally also into U2 (cols < t).
+int run_update(int64_t n, int k, const double* Q, int64_t ldq, int sx, const double* X, int64_t ldx,
+               const double* M, int ldm, int sout, const int* t_dev, double* U, int64_t ldu,
+               double* U2, int64_t ldu2, int sms, cudaStream_t st, int64_t* launches) {
+  if (n <= 0 || sout <= 0) return PQR_OK;
+  UpdateArgs a{};
+  a.Q = Q; a.ldq = ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.sx = sx; a.sout = sout;
+  a.M = M; a.ldm = ldm; a.t_dev = t_dev; a.U = U; a.ldu = ldu; a.U2 = U2; a.ldu2 = ldu2;
+  const int m = k + sx;
+  const int NT = sout > 8 ? 2 : 1;
+  const int mpad = ((m + 3) / 4) * 4;
+  const size_t smem = (size_t)NT * mpad * 8 * sizeof(double);
+  const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (sx == 0 || ((ldx & 1) == 0 && aligned16(X))) &&
+                   (ldu & 1) == 0 && aligned16(U);
+  const int64_t nslab = (n + 15) / 16;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 6, (nslab + 7) / 8));
+  const size_t smM = (size_t)NT * ((m + 7) / 8 * 8) * 8 * sizeof(double);
+  StreamGeom g = stream_geom(n, k, sx, smM, 0);
+  CUtensorMap tq, tx;
+  const bool tma_ok = vec && g.NS >= 8 && stream_smem(g, smM) <= kSmemBudget + 2048 && (sx == 0 || ((ldx & 1) == 0 && aligned16(X))) &&
+                      make_tmap(&tq, Q, n, k, ldq) && make_tmap(&tx, X, n, sx, ldx);
+  if (tma_ok) {
+    UpdTmaArgs b{};
+    b.g = g; b.sout = sout; b.M = M; b.ldm = ldm; b.t_dev = t_dev; b.U = U; b.ldu = ldu; b.U2 = U2; b.ldu2 = ldu2;
+    const size_t sm2 = stream_smem(g, smM);
+    const int g2 = (int)std::min<int64_t>(sms, (n + kSlab - 1) / kSlab);
+    if (NT == 1) {
+      cudaFuncSetAttribute(k_update_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      k_update_tma<1><<<g2, kStreamThreads, sm2, st>>>(tq, tx, b);
+    } else {
+      cudaFuncSetAttribute(k_update_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      k_update_tma<2><<<g2, kStreamThreads, sm2, st>>>(tq, tx, b);
+    }
+  } else if (NT == 1) {
+    if (vec) k_update<1, true><<<grid, kThreads, smem, st>>>(a);
+    else k_update<1, false><<<grid, kThreads, smem, st>>>(a);
+  } else {
+    if (vec) k_update<2, true><<<grid, kThreads, smem, st>>>(a);
+    else k_update<2, false><<<grid, kThreads, smem, st>>>(a);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (launches) ++*launches;
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[pqr] update launch: %s\n", cudaGetErrorString(e));
+    return PQR_ECUDA;
+  }
+  return PQR_OK;
+}
+
+int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches) {
+  k_factor<<<1, kThreads, 0, st>>>(a);
+  if (launches) ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[pqr] factor launch: %s\n", cudaGetErrorString(e));
+    return PQR_ECUDA;
+  }
+  return PQR_OK;
+}
+
+// Gram of this rank, then (nranks > 1) allgather so every rank sums all ranks'
+// partial Grams in rank order inside k_factor (bitwise identical replicas).
+int gram_and_exchange(Ctx* h, int k, int s, const double* Q, const double* X, int64_t ldx, const double** Wsum,
+                      int* nparts) {
+  const int m = k + s;
+  {
+    PROF(h, PQR_K_GRAM);
+    TRY(run_gram(h->cfg.n_local, k, s, Q, h->ld, X, ldx, h->Wloc, m, h->partials, h->ticket, h->sms, h->stream,
+                 &h->st.kernel_launches));
+  }
+  if (h->cfg.nranks > 1) {
+    PROF(h, PQR_K_NCCL);
+    NCCL_TRY(ncclAllGather(h->Wloc, h->Wall, (size_t)m * s, ncclDouble, h->comm, h->stream));
+    h->st.collectives += 1;
+    h->st.collective_bytes += (int64_t)m * s * 8;
+    *Wsum = h->Wall;
+    *nparts = h->cfg.nranks;
+  } else {
+    *Wsum = h->Wloc;
+    *nparts = 1;
+  }
+  return PQR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CholQR2 (BCGS-PIP+) solve, Alg. 8 with the recombination of DESIGN.md R1.
+// ---------------------------------------------------------------------------
+int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, double* Ud, int64_t ldud,
+                  double* Uappend, int* t_host, double tau) {
+  const int k = h->k;
+  const int m = k + s;
+  const int64_t n = h->cfg.n_local;
+  int* d_t1 = h->ints + 0;
+  int* d_t2 = h->ints + 1;
+  int* d_def = h->ints + 3;
+  const double tol2 = tau * tau;
+  const double eta = h->cfg.gram_eta > 0 ? h->cfg.gram_eta : 1e-13;
+  const bool single = (flags & PQR_SINGLE_PASS) != 0;
+
+  // pass 1: W1 = [Q X]^T X -> P1, N1, M1, t1 -> U1 = [Q X] M1
+  const double* Wsum = nullptr;
+  int nparts = 1;
+  TRY(gram_and_exchange(h, k, s, h->basis, X, ldx, &Wsum, &nparts));
+  FactorArgs f{};
+  f.W = Wsum; f.w_stride = (int64_t)m * s; f.nparts = nparts; f.ldw = m; f.k = k; f.s = s; f.s_dev = nullptr;
+  f.tol2 = tol2; f.eta = eta;
+  f.P = h->P1; f.ldp = std::max(1, k); f.N = h->N1; f.ldn = kSMax; f.M = h->M1; f.ldm = m;
+  f.t_out = d_t1; f.piv_out = h->ints + 16; f.deflated = d_def;
+  {
+    PROF(h, PQR_K_FACTOR);
+    TRY(run_factor(f, h->stream, &h->st.kernel_launches));
+  }
+  {
+    PROF(h, PQR_K_UPDATE);
+    TRY(run_update(n, k, h->basis, h->ld, s, X, ldx, h->M1, m, s, d_t1, Ud, ldud, single ? Uappend : nullptr,
+                   h->ld, h->sms, h->stream, &h->st.kernel_launches));
+  }
+  if (!single) {
+    // pass 2 on [Q U1]: W2 -> P2, N2, M2 (+ recombination) -> U = [Q U1] M2 (in place)
+    TRY(gram_and_exchange(h, k, s, h->basis, Ud, ldud, &Wsum, &nparts));
+    FactorArgs f2{};
+    f2.W = Wsum; f2.w_stride = (int64_t)m * s; f2.nparts = nparts; f2.ldw = m; f2.k = k; f2.s = s; f2.s_dev = d_t1;
+    f2.tol2 = 0.0; f2.eta = 0.0;
+    f2.P = h->P2; f2.ldp = std::max(1, k); f2.N = h->N2; f2.ldn = kSMax; f2.M = h->M2; f2.ldm = m;
+    f2.t_out = d_t2; f2.piv_out = h->ints + 32; f2.deflated = h->ints + 4;
+    f2.P1 = h->P1; f2.ldp1 = std::max(1, k); f2.N1 = h->N1; f2.ldn1 = kSMax; f2.t1_dev = d_t1; f2.s0 = s;
+    f2.Pf = h->Pf; f2.ldpf = std::max(1, k); f2.Nf = h->Nf; f2.ldnf = kSMax; f2.tf = h->ints + 2;
+    {
+      PROF(h, PQR_K_FACTOR);
+      TRY(run_factor(f2, h->stream, &h->st.kernel_launches));
+    }
+    {
+      PROF(h, PQR_K_UPDATE);
+      TRY(run_update(n, k, h->basis, h->ld, s, Ud, ldud, h->M2, m, s, d_t2, Ud, ldud, Uappend, h->ld, h->sms,
+                     h->stream, &h->st.kernel_launches));
+    }
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(h->Pf, h->P1, sizeof(double) * std::max(1, k) * s, cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(h->Nf, h->N1, sizeof(double) * kSMax * kSMax, cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(cudaMemcpyAsync(h->ints + 2, d_t1, sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+  }
+  CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  *t_host = h->h_ints[2];
+  if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;
+  return PQR_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// TSQR variant (kept in its own translation-unit-style header)
+// ===========================================================================
+#include "tsqr_api.cuh"
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* pqr_strerror(int code) {
+  switch (code) {
+    case PQR_OK: return "ok";
+    case PQR_EARG: return "invalid argument (dimension, leading dimension or null pointer)";
+    case PQR_ECAPACITY: return "capacity exceeded (k + s > k_max + s_max or s > s_max)";
+    case PQR_EBREAKDOWN: return "Cholesky breakdown / deflation needed with PQR_NO_DEFLATION";
+    case PQR_EPLAN: return "invalid TSQR block plan";
+    case PQR_ECUDA: return "CUDA error";
+    case PQR_ENCCL: return "NCCL error";
+    case PQR_ENOMEM: return "device allocation failed";
+    default: return "unknown error";
+  }
+}
+
+int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t ldq, int k) {
+  if (!out || !cfg) return PQR_EARG;
+  *out = nullptr;
+  if (cfg->n_local <= 0 || cfg->k_max < 0 || cfg->s_max < 1 || cfg->s_max > kSMax || k < 0 || k > cfg->k_max)
+    return PQR_EARG;
+  if (cfg->k_max + cfg->s_max > kMMax) return PQR_ECAPACITY;
+  if (cfg->variant != PQR_CHOLQR2 && cfg->variant != PQR_TSQR) return PQR_EARG;
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return PQR_EARG;
+  if (cfg->nranks > 1 && !cfg->nccl_id) return PQR_EARG;
+  if (k > 0 && (!Q || ldq < cfg->n_local)) return PQR_EARG;
+  if (k > cfg->n_local) return PQR_EARG;
+
+  Ctx* h = new Ctx();
+  h->cfg = *cfg;
+  h->stream = (cudaStream_t)cfg->stream;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+  h->cap = cfg->k_max + cfg->s_max;
+  h->ld = (cfg->n_local + 1) & ~int64_t(1);  // even leading dimension: 16-byte row pairs
+  const int64_t n = cfg->n_local;
+  const int sm = cfg->s_max;
+  int rc = PQR_OK;
+  auto fail = [&](int code) {
+    pqr_destroy(reinterpret_cast<pqr_handle>(h));
+    return code;
+  };
+  // small workspaces (both variants)
+  int64_t pe = 0;
+  for (int kk = 0; kk <= cfg->k_max; ++kk) pe = std::max(pe, gram_partials_needed(n, kk, sm, h->sms));
+  h->partials_elems = pe;
+  if ((rc = dalloc(&h->partials, pe))) return fail(rc);
+  if ((rc = dalloc(&h->ticket, 4))) return fail(rc);
+  if ((rc = dalloc(&h->Wloc, (size_t)h->cap * sm))) return fail(rc);
+  if ((rc = dalloc(&h->Wall, (size_t)h->cap * sm * cfg->nranks))) return fail(rc);
+  const size_t pk = (size_t)std::max(1, cfg->k_max) * sm;
+  if ((rc = dalloc(&h->P1, pk)) || (rc = dalloc(&h->P2, pk)) || (rc = dalloc(&h->Pf, pk))) return fail(rc);
+  const size_t nn = (size_t)kSMax * kSMax;
+  if ((rc = dalloc(&h->N1, nn)) || (rc = dalloc(&h->N2, nn)) || (rc = dalloc(&h->Nf, nn))) return fail(rc);
+  if ((rc = dalloc(&h->M1, (size_t)h->cap * sm)) || (rc = dalloc(&h->M2, (size_t)h->cap * sm))) return fail(rc);
+  if ((rc = dalloc(&h->ints, 64))) return fail(rc);
+  if (cudaMallocHost(&h->h_ints, 64 * sizeof(int)) != cudaSuccess) return fail(PQR_ENOMEM);
+  if (cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
+  if (cudaMemsetAsync(h->ints, 0, 64 * sizeof(int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
+
+  if (cfg->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&h->comm, cfg->nranks, id, cfg->rank);
+    if (r != ncclSuccess) {
+      fprintf(stderr, "[pqr] ncclCommInitRank: %s\n", ncclGetErrorString(r));
+      h->comm = nullptr;
+      return fail(PQR_ENCCL);
+    }
+  }
+
+  // host Q is staged through a temporary device copy
+  const double* Qd = Q;
+  double* Qtmp = nullptr;
+  int64_t ldqd = ldq;
+  if (k > 0 && is_host_ptr(Q)) {
+    if ((rc = dalloc(&Qtmp, (size_t)h->ld * k))) return fail(rc);
+    if (cudaMemcpy2DAsync(Qtmp, h->ld * sizeof(double), Q, ldq * sizeof(double), n * sizeof(double), k,
+                          cudaMemcpyHostToDevice, h->stream) != cudaSuccess) {
+      cudaFree(Qtmp);
+      return fail(PQR_ECUDA);
+    }
+    Qd = Qtmp;
+    ldqd = h->ld;
+  }
+  if (cfg->variant == PQR_CHOLQR2) {
+    if ((rc = dalloc(&h->basis, (size_t)h->ld * h->cap))) {
+      cudaFree(Qtmp);
+      return fail(rc);
+    }
+    if (k > 0 && cudaMemcpy2DAsync(h->basis, h->ld * sizeof(double), Qd, ldqd * sizeof(double), n * sizeof(double),
+                                   k, cudaMemcpyDeviceToDevice, h->stream) != cudaSuccess) {
+      cudaFree(Qtmp);
+      return fail(PQR_ECUDA);
+    }
+    h->k = k;
+  } else {
+    rc = tsqr_create(h, Qd, ldqd, k);
+    if (rc) {
+      cudaFree(Qtmp);
+      return fail(rc);
+    }
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+    cudaFree(Qtmp);
+    return fail(PQR_ECUDA);
+  }
+  cudaFree(Qtmp);
+  h->st.k = h->k;
+  *out = reinterpret_cast<pqr_handle>(h);
+  return PQR_OK;
+}
+
+int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, unsigned flags, double* U,
+                          int64_t ldu, double* P, int ldp, double* N, int ldn, int* t) {
+  Ctx* h = reinterpret_cast<Ctx*>(hh);
+  if (!h || !X || !t || s < 1) return PQR_EARG;
+  const int64_t n = h->cfg.n_local;
+  const int k = h->k;
+  if (s > h->cfg.s_max || k + s > h->cap) return PQR_ECAPACITY;
+  if (ldx < n) return PQR_EARG;
+  if (U && ldu < n) return PQR_EARG;
+  if (P && k > 0 && ldp < k) return PQR_EARG;
+  if (N && ldn < s) return PQR_EARG;
+  const bool append = !(flags & PQR_NO_APPEND);
+  if (!append && !U) return PQR_EARG;
+
+  // stage host inputs
+  const double* Xd = X;
+  int64_t ldxd = ldx;
+  if (is_host_ptr(X)) {
+    if (!h->stageX && dalloc(&h->stageX, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
+    CUDA_TRY(cudaMemcpy2DAsync(h->stageX, h->ld * sizeof(double), X, ldx * sizeof(double), n * sizeof(double), s,
+                               cudaMemcpyHostToDevice, h->stream));
+    Xd = h->stageX;
+    ldxd = h->ld;
+  }
+  const bool u_host = U && is_host_ptr(U);
+  double* Ud = nullptr;
+  int64_t ldud = 0;
+  if (U && !u_host && (ldu & 1) == 0 && aligned16(U)) {
+    Ud = U;
+    ldud = ldu;
+  } else if (!U && append && h->cfg.variant == PQR_CHOLQR2) {
+    Ud = h->basis + (int64_t)k * h->ld;  // compute in place in the basis' spare columns
+    ldud = h->ld;
+  } else {
+    if (!h->stageU && dalloc(&h->stageU, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
+    Ud = h->stageU;
+    ldud = h->ld;
+  }
+  const double tau = h->cfg.defl_tol > 0 ? h->cfg.defl_tol : 1e-12;
+  int tt = 0;
+  int rc;
+  if (h->cfg.variant == PQR_CHOLQR2) {
+    double* Uapp = (append && Ud != h->basis + (int64_t)k * h->ld) ? h->basis + (int64_t)k * h->ld : nullptr;
+    rc = cholqr2_solve(h, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
+  } else {
+    rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
+  }
+  if (rc != PQR_OK) return rc;
+  // outputs
+  if (U && Ud != U) {
+    CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, ldud * sizeof(double), n * sizeof(double), s,
+                               cudaMemcpyDefault, h->stream));
+  }
+  if (P && k > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(P, (size_t)ldp * sizeof(double), h->Pf, (size_t)std::max(1, k) * sizeof(double),
+                               (size_t)k * sizeof(double), s, cudaMemcpyDefault, h->stream));
+  if (N)
+    CUDA_TRY(cudaMemcpy2DAsync(N, (size_t)ldn * sizeof(double), h->Nf, (size_t)kSMax * sizeof(double),
+                               (size_t)s * sizeof(double), s, cudaMemcpyDefault, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  prof_collect(h);
+  *t = tt;
+  if (append) h->k += tt;
+  h->st.calls += 1;
+  h->st.k = h->k;
+  h->st.last_t = tt;
+  return PQR_OK;
+}
+
+int pqr_basis_apply(pqr_handle hh, const double* C, int ldc, int m, double* Y, int64_t ldy) {
+  Ctx* h = reinterpret_cast<Ctx*>(hh);
+  if (!h || m < 0 || !Y) return PQR_EARG;
+  const int64_t n = h->cfg.n_local;
+  const int k = h->k;
+  if (ldy < n || (k > 0 && (!C || ldc < k))) return PQR_EARG;
+  if (m == 0) return PQR_OK;
+  if (h->cfg.variant == PQR_TSQR) return tsqr_apply(h, C, ldc, m, Y, ldy);
+  // Y = Q C in chunks of <= 16 output columns (host / unaligned Y staged through stageU)
+  const bool stage = is_host_ptr(Y) || (ldy & 1) || !aligned16(Y);
+  if (stage && !h->stageU && dalloc(&h->stageU, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
+  if (!h->stageC && dalloc(&h->stageC, (size_t)h->cap * 16)) return PQR_ENOMEM;
+  const int chunk = stage ? std::min(16, h->cfg.s_max) : 16;
+  for (int c0 = 0; c0 < m; c0 += chunk) {
+    const int mc = std::min(chunk, m - c0);
+    double* dst = stage ? h->stageU : Y + (int64_t)c0 * ldy;
+    const int64_t ldd = stage ? h->ld : ldy;
+    if (k == 0) {
+      CUDA_TRY(cudaMemset2DAsync(dst, ldd * sizeof(double), 0, n * sizeof(double), mc, h->stream));
+    } else {
+      CUDA_TRY(cudaMemcpy2DAsync(h->stageC, (size_t)k * sizeof(double), C + (int64_t)c0 * ldc,
+                                 (size_t)ldc * sizeof(double), (size_t)k * sizeof(double), mc, cudaMemcpyDefault,
+                                 h->stream));
+      PROF(h, PQR_K_UPDATE);
+      TRY(run_update(n, k, h->basis, h->ld, 0, nullptr, 0, h->stageC, k, mc, nullptr, dst, ldd, nullptr, 0, h->sms,
+                     h->stream, &h->st.kernel_launches));
+    }
+    if (stage)
+      CUDA_TRY(cudaMemcpy2DAsync(Y + (int64_t)c0 * ldy, ldy * sizeof(double), h->stageU, h->ld * sizeof(double),
+                                 n * sizeof(double), mc, cudaMemcpyDefault, h->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  prof_collect(h);
+  return PQR_OK;
+}
+
+int pqr_destroy(pqr_handle hh) {
+  Ctx* h = reinterpret_cast<Ctx*>(hh);
+  if (!h) return PQR_OK;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  else cudaDeviceSynchronize();
+  tsqr_free(h);
+  cudaFree(h->basis);
+  cudaFree(h->partials);
+  cudaFree(h->ticket);
+  cudaFree(h->Wloc);
+  cudaFree(h->Wall);
+  cudaFree(h->P1); cudaFree(h->N1); cudaFree(h->M1);
+  cudaFree(h->P2); cudaFree(h->N2); cudaFree(h->M2);
+  cudaFree(h->Pf); cudaFree(h->Nf);
+  cudaFree(h->ints);
+  if (h->h_ints) cudaFreeHost(h->h_ints);
+  cudaFree(h->stageX); cudaFree(h->stageU); cudaFree(h->stageC);
+  if (h->comm) ncclCommDestroy(h->comm);
+  for (auto& p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  delete h;
+  return PQR_OK;
+}
+
+int pqr_get_stats(pqr_handle hh, pqr_stats* st) {
+  Ctx* h = reinterpret_cast<Ctx*>(hh);
+  if (!h || !st) return PQR_EARG;
+  *st = h->st;
+  return PQR_OK;
+}
+
+int pqr_profile_enable(pqr_handle hh, int enable) {
+  Ctx* h = reinterpret_cast<Ctx*>(hh);
+  if (!h) return PQR_EARG;
+  cudaStreamSynchronize(h->stream);
+  prof_collect(h);
+  h->prof = enable != 0;
+  h->prof_tot = pqr_profile{};
+  return PQR_OK;
+}
+
+int pqr_get_profile(pqr_handle hh, pqr_profile* out) {
+  Ctx* h = reinterpret_cast<Ctx*>(hh);
+  if (!h || !out) return PQR_EARG;
+  cudaStreamSynchronize(h->stream);
+  prof_collect(h);
+  *out = h->prof_tot;
+  return PQR_OK;
+}
+
+int pqr_nccl_unique_id(void* id128) {
+  if (!id128) return PQR_EARG;
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id128, &id, sizeof(id));
+  return PQR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// step-level entry points (include/pqr_steps.h)
+// ---------------------------------------------------------------------------
+int pqr_step_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double* X, int64_t ldx, double* W,
+                  int ldw, void* stream) {
+  if (n <= 0 || k < 0 || s < 1 || s > kSMax || k + s > kMMax || !X || ldx < n || (k > 0 && (!Q || ldq < n)) ||
+      !W || ldw < k + s)
+    return PQR_EARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* part = nullptr;
+  unsigned int* ticket = nullptr;
+  if (dalloc(&part, gram_partials_needed(n, k, s, sms)) || dalloc(&ticket, 1)) {
+    cudaFree(part);
+    return PQR_ENOMEM;
+  }
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st);
+  int rc = run_gram(n, k, s, Q, ldq, X, ldx, W, ldw, part, ticket, sms, st, nullptr);
+  cudaStreamSynchronize(st);
+  cudaFree(part);
+  cudaFree(ticket);
+  return rc ? rc : (cudaGetLastError() == cudaSuccess ? PQR_OK : PQR_ECUDA);
+}
+
+int pqr_step_factor(int k, int s, const double* W, int ldw, double tol2_rel, double eta, double* N, int ldn,
+                    double* M, int ldm, int* t_host, int* piv_host, void* stream) {
+  if (k < 0 || s < 1 || s > kSMax || k + s > kMMax || !W || ldw < k + s || !N || ldn < s || !M || ldm < k + s ||
+      !t_host)
+    return PQR_EARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  double *P = nullptr, *Nt = nullptr;
+  int* ints = nullptr;
+  if (dalloc(&P, (size_t)std::max(1, k) * s) || dalloc(&Nt, kSMax * kSMax) || dalloc(&ints, 64)) {
+    cudaFree(P);
+    cudaFree(Nt);
+    return PQR_ENOMEM;
+  }
+  FactorArgs f{};
+  f.W = W; f.w_stride = 0; f.nparts = 1; f.ldw = ldw; f.k = k; f.s = s; f.tol2 = tol2_rel; f.eta = eta;
+  f.P = P; f.ldp = std::max(1, k); f.N = Nt; f.ldn = kSMax; f.M = M; f.ldm = ldm;
+  f.t_out = ints; f.piv_out = ints + 16; f.deflated = ints + 1;
+  int rc = run_factor(f, st, nullptr);
+  int hbuf[32];
+  if (!rc) {
+    cudaMemcpy2DAsync(N, ldn * sizeof(double), Nt, kSMax * sizeof(double), s * sizeof(double), s, cudaMemcpyDefault,
+                      st);
+    cudaMemcpyAsync(hbuf, ints, 32 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = PQR_ECUDA;
+  }
+  if (!rc) {
+    *t_host = hbuf[0];
+    if (piv_host)
+      for (int i = 0; i < s; ++i) piv_host[i] = hbuf[16 + i];
+  }
+  cudaFree(P);
+  cudaFree(Nt);
+  cudaFree(ints);
+  return rc;
+}
+
+int pqr_step_update(int64_t n, int k, int s, const double* Q, int64_t ldq, const double* X, int64_t ldx,
+                    const double* M, int ldm, int t, double* U, int64_t ldu, void* stream) {
+  if (n <= 0 || k < 0 || s < 1 || s > kSMax || t < 0 || t > s || k + s > kMMax || !X || ldx < n ||
+      (k > 0 && (!Q || ldq < n)) || !M || ldm < k + s || !U || ldu < n)
+    return PQR_EARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int* td = nullptr;
+  if (dalloc(&td, 1)) return PQR_ENOMEM;
+  cudaMemcpyAsync(td, &t, sizeof(int), cudaMemcpyHostToDevice, st);
+  int rc = run_update(n, k, Q, ldq, s, X, ldx, M, ldm, s, td, U, ldu, nullptr, 0, sms, st, nullptr);
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = PQR_ECUDA;
+  cudaFree(td);
+  return rc;
+}
+
+}  // extern "C"

@@ -138,20 +138,29 @@ def device_gaussian(seed: int, n: int, m: int, device) -> "torch.Tensor":
     return out
 
 
-def device_orthonormal(seed: int, n: int, k: int, device, scale: float = 1.0) -> "torch.Tensor":
-    """Orthonormal factor (cuSOLVER QR via torch.linalg.qr) of a seeded Gaussian, column-major.
-    ``scale`` = 1/sqrt(P) makes P independently drawn row shards globally orthonormal."""
+def device_orthonormal(seed: int, n: int, k: int, device, scale: float = 1.0, slab: int = 2 ** 21) -> "torch.Tensor":
+    """Orthonormal n x k (column-major) from a seeded Gaussian via cuSOLVER QR (torch.linalg.qr).
+
+    For n > slab the rows are cut into c = ceil(n/slab) slabs, each slab's Gaussian is
+    QR-factorised on its own and the stacked factors are scaled by 1/sqrt(c):
+    sum_i (Q_i/sqrt(c))^T (Q_i/sqrt(c)) = I, so the result is globally orthonormal
+    (cuSOLVER's orgqr fails beyond ~2^31 elements).  ``scale`` multiplies the result
+    (1/sqrt(P) makes P independently drawn rank shards globally orthonormal)."""
     torch = _torch()
-    if k == 0:
-        return colmajor_empty(n, 0, device)
-    A = device_gaussian(seed, n, k, device)
-    q, _ = torch.linalg.qr(A, mode="reduced")
-    del A
     out = colmajor_empty(n, k, device)
-    out.copy_(q)
-    del q
-    if scale != 1.0:
-        out.mul_(scale)
+    if k == 0:
+        return out
+    c = max(1, -(-n // slab))
+    bounds = [(i * n // c, (i + 1) * n // c) for i in range(c)]
+    for i, (r0, r1) in enumerate(bounds):
+        A = device_gaussian(seed + 7919 * i, r1 - r0, k, device)
+        q, _ = torch.linalg.qr(A, mode="reduced")
+        del A
+        out[r0:r1].copy_(q)
+        del q
+    f = scale / math.sqrt(c)
+    if f != 1.0:
+        out.mul_(f)
     return out
 
 

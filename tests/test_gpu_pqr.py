@@ -1,0 +1,201 @@
+"""GPU parity of pqr_project_normalize / pqr_basis_apply end to end (both variants,
+all §8(a) rows through the C-ABI) against the CPU oracle.
+
+Tolerances (BASELINE north_star): relative Frobenius error of U, P, N <= 1e-10 for
+kappa <= 1e4 and ||I - [Q U]^T [Q U]||_2 <= 1e-12."""
+import numpy as np
+import pytest
+
+from gpu_util import dev, empty, host, ortho_loss_2, rel
+from paper_2204_13393_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+VARIANTS = ["cholqr2", "tsqr"]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2204_13393_b200 import pqr
+
+    pqr.lib()
+    return pqr
+
+
+# ---------------------------------------------------------------------------
+# end to end (a1-a5 through pqr_project_normalize)
+# ---------------------------------------------------------------------------
+def solve(P, Q, X, variant="cholqr2", flags=None, k_max=None, **kw):
+    import torch
+
+    n, s = X.shape
+    k = Q.shape[1]
+    Qd, Xd = dev(Q), dev(X)
+    U, Pm, Nm = empty(n, s), empty(max(k, 1), s), empty(s, s)
+    with P.PQR(n, k_max or k, s, Qd if k else None, k=k, variant=variant, **kw) as h:
+        t = h.solve(Xd, U=U, P=Pm, N=Nm, flags=P.PQR_NO_APPEND if flags is None else flags)
+        st = h.stats()
+    torch.cuda.synchronize()
+    return dict(U=host(U)[:, :t], P=host(Pm)[:k], N=host(Nm), t=t, stats=st, Qd=Qd, Ud=U[:, :t])
+
+
+def check_vs_oracle(out, ref, tol=1e-10):
+    assert out["t"] == ref["t"]
+    if ref["P"].size:
+        assert rel(out["P"], ref["P"]) < tol
+    assert rel(out["N"], ref["N"]) < tol
+    assert rel(out["U"], ref["U"]) < tol
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("n,k,s", [(10_000, 32, 4), (4097, 13, 3), (20_000, 0, 8), (65_536, 128, 8),
+                                   (30_001, 96, 16), (12, 3, 2), (300_007, 64, 8)])
+def test_vs_oracle_random(P, orc, variant, n, k, s):
+    Q = inputs.orthonormal(7 + n, n, k)
+    X = inputs.gaussian(8 + n, n, s)
+    out = solve(P, Q, X, variant=variant)
+    ref = orc.householder_pqr(Q, X)
+    check_vs_oracle(out, ref)
+    assert ortho_loss_2(out["Qd"], out["Ud"]) < 1e-12
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_tiny_config(P, orc, variant):
+    """configs[0] at full size: n=10,000, k=32, s=4."""
+    Q, X = inputs.tiny_inputs()
+    out = solve(P, Q, X, variant=variant)
+    check_vs_oracle(out, orc.householder_pqr(Q, X))
+    assert ortho_loss_2(out["Qd"], out["Ud"]) < 1e-12
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_projected(P, orc, variant):
+    """configs[1] shape (projection dominates, reading R8) at n = 2^18."""
+    Q, X = inputs.projected_inputs(21, 2 ** 18, 64, 8)
+    out = solve(P, Q, X, variant=variant)
+    check_vs_oracle(out, orc.householder_pqr(Q, X))
+    assert ortho_loss_2(out["Qd"], out["Ud"]) < 1e-12
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_manufactured(P, variant):
+    m = inputs.manufactured(31, 2 ** 16, 64, 8)
+    out = solve(P, m["Q"], m["X"], variant=variant)
+    assert out["t"] == 8
+    assert rel(out["P"], m["C"]) < 1e-12 and rel(out["N"], m["D"]) < 1e-11 and rel(out["U"], m["Y"]) < 1e-10
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_special_cases(P, variant):
+    n, k, s = 5000, 16, 4
+    m = inputs.manufactured(41, n, k, s)
+    # X orthonormal and orthogonal to Q: P = 0, N = I, U = X
+    out = solve(P, m["Q"], m["Y"], variant=variant)
+    assert np.linalg.norm(out["P"]) < 1e-13 and rel(out["N"], np.eye(s)) < 1e-13 and rel(out["U"], m["Y"]) < 1e-13
+    # X inside span(Q): t = 0, P = C
+    out = solve(P, m["Q"], np.asfortranarray(m["Q"] @ m["C"]), variant=variant)
+    assert out["t"] == 0 and rel(out["P"], m["C"]) < 1e-13 and np.all(out["N"] == 0)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_deflation_small(P, orc, variant):
+    """configs[3] shape at n = 2^15: two dependent columns -> t = 14, pivots as the oracle."""
+    Q, X = inputs.deflation_inputs(51, 2 ** 15, 96, 16)
+    ref = orc.householder_pqr(Q, X)
+    assert ref["t"] == 14
+    out = solve(P, Q, X, variant=variant)
+    assert out["t"] == 14
+    assert rel(out["P"], ref["P"]) < 1e-10
+    # N row-echelon with the oracle's pivot columns; projectors agree
+    piv = [int(np.flatnonzero(np.abs(ref["N"][i]) > 0)[0]) for i in range(14)]
+    piv_gpu = [int(np.flatnonzero(np.abs(out["N"][i]) > 0)[0]) for i in range(14)]
+    assert piv == piv_gpu
+    assert np.all(out["N"][14:] == 0)
+    Pu = out["U"] @ out["U"].T[:, :64]
+    Pr = ref["U"] @ ref["U"].T[:, :64]
+    assert rel(Pu, Pr) < 1e-6
+
+
+def test_cholqr2_single_pass_is_bcgs_pip(P, orc):
+    """PQR_SINGLE_PASS = Alg. 7 (one BCGS-PIP pass): same result as the oracle's Alg. 7."""
+    Q, X = inputs.projected_inputs(61, 20_000, 32, 4, ratio=1e-2)
+    out = solve(P, Q, X, flags=P.PQR_NO_APPEND | P.PQR_SINGLE_PASS)
+    ref = orc.bcgs_pip(Q, X)
+    assert out["t"] == ref["t"]
+    assert rel(out["P"], ref["P"]) < 1e-12 and rel(out["N"], ref["N"]) < 1e-10 and rel(out["U"], ref["U"]) < 1e-9
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_append_and_basis_apply(P, orc, variant):
+    """Append semantics (Alg. 1): after two solves k = k0 + 2s; Y = Q C reproduces the basis."""
+    import torch
+
+    n, k0, s = 9000, 8, 4
+    Q = inputs.orthonormal(71, n, k0)
+    X1 = inputs.gaussian(72, n, s)
+    X2 = inputs.gaussian(73, n, s)
+    with P.PQR(n, k0 + 2 * s, s, dev(Q), variant=variant) as h:
+        t1 = h.solve(dev(X1))
+        t2 = h.solve(dev(X2))
+        assert (t1, t2) == (s, s) and h.k == k0 + 2 * s
+        C = np.eye(k0 + 2 * s)
+        Y = empty(n, k0 + 2 * s)
+        h.apply(dev(C), k0 + 2 * s, Y)
+        torch.cuda.synchronize()
+        B = host(Y)
+    ref1 = orc.householder_pqr(Q, X1)
+    Q1 = np.hstack([Q, ref1["U"]])
+    ref2 = orc.householder_pqr(Q1, X2)
+    assert rel(B[:, :k0], Q) < 1e-13
+    assert rel(B[:, k0:k0 + s], ref1["U"]) < 1e-10
+    assert rel(B[:, k0 + s:], ref2["U"]) < 1e-10
+    # general C: Y = Q C
+    C = inputs.gaussian(74, k0 + 2 * s, 5)
+    with P.PQR(n, k0, s, dev(Q), variant=variant) as h:
+        Y = empty(n, 5)
+        h.apply(dev(C[:k0]), 5, Y)
+        torch.cuda.synchronize()
+        assert rel(host(Y), orc.matmul(Q, C[:k0])) < 1e-13
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_host_buffers(P, orc, variant):
+    """Host (numpy) X/U/P/N go through the library's staging (the e2e path)."""
+    n, k, s = 6000, 12, 4
+    Q = inputs.orthonormal(81, n, k)
+    X = inputs.gaussian(82, n, s)
+    U = np.zeros((n, s), order="F")
+    Pm = np.zeros((k, s), order="F")
+    Nm = np.zeros((s, s), order="F")
+    with P.PQR(n, k, s, Q, variant=variant) as h:
+        t = h.solve(X, U=U, P=Pm, N=Nm, flags=P.PQR_NO_APPEND)
+    ref = orc.householder_pqr(Q, X)
+    assert t == s
+    assert rel(Pm, ref["P"]) < 1e-10 and rel(Nm, ref["N"]) < 1e-10 and rel(U, ref["U"]) < 1e-10
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_no_deflation_flag_breakdown(P, variant):
+    n, k, s = 4000, 8, 4
+    Q = inputs.orthonormal(91, n, k)
+    X = inputs.gaussian(92, n, s)
+    X[:, 2] = X[:, 0]
+    with P.PQR(n, k, s, dev(Q), variant=variant) as h:
+        with pytest.raises(P.PQRError) as e:
+            h.solve(dev(X), flags=P.PQR_NO_DEFLATION)
+        assert e.value.code == P.PQR_EBREAKDOWN
+        assert h.k == k  # basis unchanged on error
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_capacity_error(P, variant):
+    n = 1000
+    with P.PQR(n, 4, 4, None, k=0, variant=variant) as h:
+        X = dev(inputs.gaussian(1, n, 4))
+        assert h.solve(X) == 4 and h.solve(X) == 0  # second block is in span -> t = 0
+        with pytest.raises(P.PQRError) as e:
+            h.solve(dev(inputs.gaussian(2, n, 8)))
+        assert e.value.code == P.PQR_ECAPACITY
