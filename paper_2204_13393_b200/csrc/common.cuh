@@ -93,3 +93,50 @@ PQR_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 }
 
 }  // namespace pqr
+
+// ---------------------------------------------------------------------------
+// cp.async (LDGSTS) 16-byte global->shared copies with zero fill
+// ---------------------------------------------------------------------------
+namespace pqr {
+// copies `src_bytes` (0, 8 or 16) bytes and zero-fills the rest of the 16-byte chunk
+PQR_DEV void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+PQR_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+PQR_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+}  // namespace pqr
+
+namespace pqr {
+// wait until at most n of this thread's most recent cp.async groups are pending (n <= 14)
+PQR_DEV void cp_async_wait_dyn(int n) {
+  switch (n) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 4: cp_async_wait<4>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 6: cp_async_wait<6>(); break;
+    case 7: cp_async_wait<7>(); break;
+    case 8: cp_async_wait<8>(); break;
+    case 9: cp_async_wait<9>(); break;
+    case 10: cp_async_wait<10>(); break;
+    case 11: cp_async_wait<11>(); break;
+    case 12: cp_async_wait<12>(); break;
+    case 13: cp_async_wait<13>(); break;
+    default: cp_async_wait<14>(); break;
+  }
+}
+}  // namespace pqr
+
+namespace pqr {
+// the mbarrier receives one (non-incrementing) arrival once all of this thread's prior
+// cp.async copies have landed
+PQR_DEV void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+}  // namespace pqr

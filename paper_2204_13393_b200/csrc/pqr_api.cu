@@ -210,65 +210,11 @@ cudaError_t launch_gram_mtw(const GramPlan& p, const GramArgs& a, bool vec, cuda
 
 constexpr int kSmemBudget = 225 * 1024;
 
-// ---- TMA tensor maps (driver entry point fetched through the runtime) ----
-typedef CUresult (*PFN_tmapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-PFN_tmapEncodeTiled tmap_encoder() {
-  static PFN_tmapEncodeTiled fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_tmapEncodeTiled>(p);
-    else
-      cudaGetLastError();
-  }
-  return fn;
-}
-// rows x cols column-major fp64 (ld even, base 16-B aligned); box = kSlab rows x cols, no swizzle,
-// out-of-bounds rows read as zero.
-bool make_tmap(CUtensorMap* tm, const double* base, int64_t rows, int cols, int64_t ld) {
-  memset(tm, 0, sizeof(*tm));
-  if (cols <= 0) return true;
-  PFN_tmapEncodeTiled enc = tmap_encoder();
-  if (!enc || cols > 256) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-  cuuint32_t box[2] = {(cuuint32_t)kSlab, (cuuint32_t)cols};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
-StreamGeom stream_geom(int64_t n, int k, int sx, size_t extra_bytes, size_t min_stage_region) {
-  StreamGeom g{};
-  g.n = n; g.k = k; g.sx = sx;
-  g.k8 = (k + 7) / 8 * 8;
-  g.x8 = (sx + 7) / 8 * 8;
-  g.stage_dbl = (g.k8 + g.x8) * kSlab;
-  const size_t stage_bytes = (size_t)g.stage_dbl * sizeof(double);
-  // NS must be a multiple of the consumer-warp count: warp w owns stages w, w+8, ... so a
-  // warp never waits on a stage more than one mbarrier phase ahead (parity waits).
-  const size_t avail = kSmemBudget - 1024 - extra_bytes;
-  const int R = (int)std::max<size_t>(1, std::min<size_t>(3, avail / (kStreamConsumers * (stage_bytes + 16))));
-  g.NS = kStreamConsumers * R;
-  if ((size_t)g.NS * stage_bytes < min_stage_region) g.NS = 0;  // reduction would not fit: no TMA path
-  return g;
-}
-size_t stream_smem(const StreamGeom& g, size_t extra_bytes) {
-  return 1024 + (size_t)g.NS * g.stage_dbl * sizeof(double) + 2 * g.NS * sizeof(uint64_t) + extra_bytes;
-}
-
-template <int MTMAX, int NT>
-cudaError_t launch_gram_tma_t(int grid, size_t smem, const CUtensorMap& tq, const CUtensorMap& tx,
-                              const GramTmaArgs& a, cudaStream_t st) {
-  auto f = k_gram_tma<MTMAX, NT>;
+template <int MTH, int NT, int RB>
+cudaError_t launch_gram_cpa_t(int grid, size_t smem, const GramCpaArgs& a, cudaStream_t st) {
+  auto f = k_gram_cpa<MTH, NT, RB>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  f<<<grid, kStreamThreads, smem, st>>>(tq, tx, a);
+  f<<<grid, kCpaThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -277,30 +223,35 @@ int run_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double
              double* W, int ldw, double* partials, unsigned int* ticket, int sms, cudaStream_t st,
              int64_t* launches) {
   const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (ldx & 1) == 0 && aligned16(X);
-  const int m = k + s, MT = (m + 7) / 8;
-  const size_t red_bytes = (size_t)kStreamConsumers * MT * (s > 8 ? 2 : 1) * 64 * sizeof(double);
-  StreamGeom g = stream_geom(n, k, s, 0, red_bytes);
-  CUtensorMap tq, tx;
-  const bool tma = vec && MT <= 20 && g.NS >= 8 && stream_smem(g, 0) <= kSmemBudget + 2048 &&
-                   make_tmap(&tq, Q, n, k, ldq) && make_tmap(&tx, X, n, s, ldx);
+  static const int env_rb = getenv("PQR_GRAM_RB") ? atoi(getenv("PQR_GRAM_RB")) : 32;
+  static const int env_ctas = getenv("PQR_GRAM_CTAS") ? atoi(getenv("PQR_GRAM_CTAS")) : 1;
+  const int RB = env_rb == 32 ? 32 : 16;
+  const int ctas = env_ctas == 1 ? 1 : 2;
+  const int groups = kCpaWarps / (RB / 8);
+  const int m = k + s, MT = (m + 7) / 8, MTH = (MT + groups - 1) / groups, NT = s > 8 ? 2 : 1;
+  const size_t stage_bytes = (size_t)MT * 8 * (RB + 8) * sizeof(double);
+  const size_t red_bytes = (size_t)kCpaWarps * MTH * NT * 64 * sizeof(double);
+  const size_t budget = ctas == 2 ? kSmemBudget / 2 - 2048 : kSmemBudget;
+  int NS = (int)std::min<size_t>(8, budget / (stage_bytes + 16));
+  while (NS >= 2 && (size_t)NS * stage_bytes < red_bytes) ++NS;
+  const size_t smem = std::max((size_t)NS * stage_bytes, red_bytes) + 2 * NS * sizeof(uint64_t);
   cudaError_t e;
-  if (tma) {
-    GramTmaArgs a{};
-    a.g = g; a.partials = partials; a.W = W; a.ldw = ldw; a.ticket = ticket;
-    const size_t smem = stream_smem(g, 0);
-    const int grid = (int)std::min<int64_t>(sms, (n + kSlab - 1) / kSlab);
-    const int NT = s > 8 ? 2 : 1;
-    const int MB = MT <= 5 ? 5 : (MT <= 10 ? 10 : (MT <= 15 ? 15 : 20));
-    switch (MB * 10 + NT) {
-      case 51: e = launch_gram_tma_t<5, 1>(grid, smem, tq, tx, a, st); break;
-      case 52: e = launch_gram_tma_t<5, 2>(grid, smem, tq, tx, a, st); break;
-      case 101: e = launch_gram_tma_t<10, 1>(grid, smem, tq, tx, a, st); break;
-      case 102: e = launch_gram_tma_t<10, 2>(grid, smem, tq, tx, a, st); break;
-      case 151: e = launch_gram_tma_t<15, 1>(grid, smem, tq, tx, a, st); break;
-      case 152: e = launch_gram_tma_t<15, 2>(grid, smem, tq, tx, a, st); break;
-      case 201: e = launch_gram_tma_t<20, 1>(grid, smem, tq, tx, a, st); break;
-      default: e = launch_gram_tma_t<20, 2>(grid, smem, tq, tx, a, st); break;
+  if (vec && MTH <= 10 && NS >= 3 && smem <= budget) {
+    GramCpaArgs a{};
+    a.Q = Q; a.ldq = ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.NS = NS;
+    a.partials = partials; a.W = W; a.ldw = ldw; a.ticket = ticket;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * ctas, (n + RB - 1) / RB));
+#define PQR_GRAM_CASE(H)                                                                                    \
+  case H * 100 + 10 + 1: e = launch_gram_cpa_t<H, 1, 16>(grid, smem, a, st); break;                       \
+  case H * 100 + 10 + 2: e = launch_gram_cpa_t<H, 2, 16>(grid, smem, a, st); break;                       \
+  case H * 100 + 20 + 1: e = launch_gram_cpa_t<H, 1, 32>(grid, smem, a, st); break;                       \
+  case H * 100 + 20 + 2: e = launch_gram_cpa_t<H, 2, 32>(grid, smem, a, st); break;
+    switch (MTH * 100 + (RB / 16) * 10 + NT) {
+      PQR_GRAM_CASE(1) PQR_GRAM_CASE(2) PQR_GRAM_CASE(3) PQR_GRAM_CASE(4) PQR_GRAM_CASE(5)
+      PQR_GRAM_CASE(6) PQR_GRAM_CASE(7) PQR_GRAM_CASE(8) PQR_GRAM_CASE(9) PQR_GRAM_CASE(10)
+      default: e = cudaErrorInvalidValue; break;
     }
+#undef PQR_GRAM_CASE
   } else {
     const GramPlan p = plan_gram(n, k, s, sms);
     GramArgs a{};
@@ -318,7 +269,7 @@ int run_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double
 
 int64_t gram_partials_needed(int64_t n, int k, int s, int sms) {
   const GramPlan p = plan_gram(n, k, s, sms);
-  return (int64_t)std::max(p.grid, sms) * (k + s) * s;
+  return (int64_t)std::max(p.grid, 2 * sms) * (k + s) * s;
 }
 
 // U (cols < sout) = [Q X] M, optionally also into U2 (cols < t).
@@ -337,22 +288,30 @@ int run_update(int64_t n, int k, const double* Q, int64_t ldq, int sx, const dou
                    (ldu & 1) == 0 && aligned16(U);
   const int64_t nslab = (n + 15) / 16;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 6, (nslab + 7) / 8));
-  const size_t smM = (size_t)NT * ((m + 7) / 8 * 8) * 8 * sizeof(double);
-  StreamGeom g = stream_geom(n, k, sx, smM, 0);
-  CUtensorMap tq, tx;
-  const bool tma_ok = vec && g.NS >= 8 && stream_smem(g, smM) <= kSmemBudget + 2048 && (sx == 0 || ((ldx & 1) == 0 && aligned16(X))) &&
-                      make_tmap(&tq, Q, n, k, ldq) && make_tmap(&tx, X, n, sx, ldx);
-  if (tma_ok) {
-    UpdTmaArgs b{};
-    b.g = g; b.sout = sout; b.M = M; b.ldm = ldm; b.t_dev = t_dev; b.U = U; b.ldu = ldu; b.U2 = U2; b.ldu2 = ldu2;
-    const size_t sm2 = stream_smem(g, smM);
-    const int g2 = (int)std::min<int64_t>(sms, (n + kSlab - 1) / kSlab);
+  static const int env_cw = getenv("PQR_UPD_CW") ? atoi(getenv("PQR_UPD_CW")) : 16;
+  static const int env_ctas = getenv("PQR_UPD_CTAS") ? atoi(getenv("PQR_UPD_CTAS")) : 2;
+  const int CW = env_cw == 16 ? 16 : 32;
+  const int ctas = env_ctas == 2 ? 2 : 1;
+  const int nch = (m + CW - 1) / CW;
+  const size_t smM = (size_t)NT * nch * CW * 8 * sizeof(double);
+  const size_t stg = (size_t)CW * kUpdRBP * sizeof(double);
+  const size_t budget = ctas == 2 ? kSmemBudget / 2 - 2048 : kSmemBudget;
+  const int NS = smM + 3 * stg < budget ? (int)std::min<size_t>(12, (budget - smM) / (stg + 16)) : 0;
+  const bool cpa_ok = vec && NS >= 3 && (sx == 0 || ((ldx & 1) == 0 && aligned16(X)));
+  if (cpa_ok) {
+    UpdCpaArgs b{};
+    b.Q = Q; b.ldq = ldq; b.X = X; b.ldx = ldx; b.n = n; b.k = k; b.sx = sx; b.sout = sout;
+    b.M = M; b.ldm = ldm; b.t_dev = t_dev; b.U = U; b.ldu = ldu; b.U2 = U2; b.ldu2 = ldu2; b.NS = NS;
+    const size_t sm2 = smM + NS * stg + 2 * NS * sizeof(uint64_t);
+    const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * ctas, (n + kUpdRB - 1) / kUpdRB));
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      kern<<<g2, kCpaThreads, sm2, st>>>(b);
+    };
     if (NT == 1) {
-      cudaFuncSetAttribute(k_update_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-      k_update_tma<1><<<g2, kStreamThreads, sm2, st>>>(tq, tx, b);
+      if (CW == 16) go(k_update_cpa<1, 16>); else go(k_update_cpa<1, 32>);
     } else {
-      cudaFuncSetAttribute(k_update_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-      k_update_tma<2><<<g2, kStreamThreads, sm2, st>>>(tq, tx, b);
+      if (CW == 16) go(k_update_cpa<2, 16>); else go(k_update_cpa<2, 32>);
     }
   } else if (NT == 1) {
     if (vec) k_update<1, true><<<grid, kThreads, smem, st>>>(a);

@@ -1,194 +1,196 @@
-// stream_kernels.cuh — TMA-pipelined CholQR2 passes (§8(a) a1 Gram, a4 update).
+// stream_kernels.cuh — pipelined CholQR2 passes (§8(a) a1 Gram, a4 update).
 //
-// One persistent CTA per SM (grid = #SMs), 9 warps:
-//   warp 8 (producer, one elected lane) streams 8-row slabs of [Q X] into a ring of
-//     NS shared-memory stages with 2-D TMA tensor copies (cp.async.bulk.tensor, SASS
-//     UTMALDG): one box of 8 rows x k columns of Q and one of 8 rows x s columns of X
-//     per slab; out-of-bounds rows are zero-filled by the TMA unit (so a ragged last
-//     slab needs no special path);
-//   warps 0..7 (consumers): warp w owns stages w, w+8, ..., w+8(R-1) and the slabs
-//     that land in them; it waits on the stage's `full` mbarrier (transaction bytes),
-//     computes with fp64 MMAs (mma.sync m8n8k4 .f64 = DMMA.8x8x4) and releases the
-//     stage on its `empty` mbarrier.  Owning stages makes every parity wait at most
-//     one phase ahead of the barrier.
-// NS = 8R stages of (k+s) x 64 B (R = 2-3) keep ~100-200 KB of loads in flight per SM
-// (Little's law at ~7 TB/s) without spending registers on it.
+// Design (measured, see DESIGN.md §6 and profiles/r01_*):
+//  * A memory-bound fp64 stream needs ~100-200 KB of loads in flight per SM.  The
+//    kernels keep NS-1 shared-memory stages in flight with cp.async (LDGSTS, 16 B per
+//    thread, zero-fill past n); each stage's arrival is tracked by an mbarrier that
+//    every thread arms with cp.async.mbarrier.arrive.noinc, and one barrier per stage
+//    protects stage reuse.  One persistent 256-thread CTA per SM.  The per-thread copy
+//    tasks are fixed across stages (shifts only, no divisions in the loop).
+//  * TMA tensor copies were measured and rejected for this layout: on B200 the TMA
+//    unit moves about one box line per ~8 SM cycles, and a line is one column's run
+//    of rows (column-major data): 64/128/256/512-byte lines stream at 2.3/4.6/6.6/7.2
+//    TB/s (tools/tma_bench.cu), and long lines cannot be swizzled, so the MMA fragment
+//    reads (8 columns x 4 row pairs, or 4 columns x 8 row pairs) would hit 2-4-way
+//    bank conflicts.  cp.async lets each stage use a padded column stride that makes
+//    both fragment patterns conflict-free.
+//  * Compute: fp64 mma.sync m8n8k4 (DMMA.8x8x4), fragments read with LDS.128.
 //
-// A stage line is one column's 8 rows (64 B, no swizzle): the Gram A fragment (8
-// columns x 4 row pairs) reads 512 contiguous bytes and the update B fragment (4
-// columns x 8 rows) 256 contiguous bytes, both bank-conflict-free.
+// k_gram_cpa    W = [Q X]^T X.  Stage = 32 rows x all m columns;
+//               warp w handles 8-row sub-slab (w & 3) of every stage for half
+//               (w >> 2) of the column tiles; sub-slab warps are summed in fixed order.
+// k_update_cpa  U = [Q X] M.  Stage = 128 rows x 16 columns;
+//               warp w owns the 16-row unit w of a row block and accumulates U^T over
+//               the column chunks in registers.
 #pragma once
-#include <cuda.h>
-
 #include "cholqr_kernels.cuh"
 #include "common.cuh"
 
 namespace pqr {
 
-constexpr int kStreamConsumers = 8;
-constexpr int kStreamThreads = (kStreamConsumers + 1) * 32;
-constexpr int kSlab = 8;  // rows per stage
+constexpr int kCpaThreads = 256;
+constexpr int kCpaWarps = kCpaThreads / 32;
 
 PQR_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
-PQR_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-PQR_DEV void tma_prefetch_desc(const CUtensorMap* tm) {
-  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
-}
-
-// Stage layout: Q box lines 0..k-1 (region padded to k8 lines), then X box lines;
-// line r holds the slab's 8 rows of one column.  Returns &column j of [Q X], row `row`.
-PQR_DEV const double* frag_ptr(const double* stage, int j, int k, int k8, int row) {
-  const int r = j < k ? j : k8 + (j - k);
-  return stage + r * kSlab + row;
-}
-
-struct StreamGeom {
-  int64_t n;
-  int k, sx;      // columns of Q and X
-  int k8, x8;     // padded line counts (multiples of 8)
-  int NS;         // stages
-  int stage_dbl;  // doubles per stage = (k8 + x8) * 8
-};
-
-// shared-memory carve-up: [align 1024][NS stages][full NS][empty NS]
-struct StreamSmem {
-  double* stages;
-  uint64_t* full;
-  uint64_t* empty;
-};
-PQR_DEV StreamSmem carve(double* raw, const StreamGeom& g) {
-  StreamSmem s;
-  const uint32_t base = smem_u32(raw);
-  const uint32_t aligned = (base + 1023u) & ~1023u;
-  s.stages = raw + (aligned - base) / sizeof(double);
-  s.full = reinterpret_cast<uint64_t*>(s.stages + (size_t)g.NS * g.stage_dbl);
-  s.empty = s.full + g.NS;
-  return s;
-}
-
-PQR_DEV void stream_init(const StreamSmem& s, const StreamGeom& g, const CUtensorMap* tmQ, const CUtensorMap* tmX) {
-  // padding lines are never written by the TMA: zero every stage once
-  for (int e = threadIdx.x; e < g.NS * g.stage_dbl; e += blockDim.x) s.stages[e] = 0.0;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < g.NS; ++i) {
-      mbar_init(&s.full[i], 1);
-      mbar_init(&s.empty[i], 1);
-    }
-    fence_mbar_init();
-    if (g.k > 0) tma_prefetch_desc(tmQ);
-    if (g.sx > 0) tma_prefetch_desc(tmX);
-  }
-  fence_proxy_async_smem();
-  __syncthreads();
-}
-
-// Producer loop: slab i = blockIdx.x + j*gridDim.x goes to stage j % NS.
-PQR_DEV void stream_produce(const StreamSmem& s, const StreamGeom& g, const CUtensorMap* tmQ, const CUtensorMap* tmX) {
-  const int64_t nsl = (g.n + kSlab - 1) / kSlab;
-  const uint32_t bytes = (uint32_t)(g.k + g.sx) * kSlab * 8u;
-  int j = 0;
-  for (int64_t sl = blockIdx.x; sl < nsl; sl += gridDim.x, ++j) {
-    const int st = j % g.NS;
-    mbar_wait(&s.empty[st], ((uint32_t)(j / g.NS) & 1u) ^ 1u);
-    mbar_arrive_expect_tx(&s.full[st], bytes);
-    double* stage = s.stages + (size_t)st * g.stage_dbl;
-    const int row0 = (int)(sl * kSlab);
-    if (g.k > 0) tma_load_2d(stage, tmQ, row0, 0, &s.full[st]);
-    if (g.sx > 0) tma_load_2d(stage + g.k8 * kSlab, tmX, row0, 0, &s.full[st]);
-  }
+// 16-byte chunk of rows (row, row+1) of a column, zero-filled past n (or for a missing
+// column: colp == nullptr).  `safe` is any valid global address (not read when 0 bytes).
+PQR_DEV void cp_rows(double* dst, const double* colp, int64_t row, int64_t n, const double* safe) {
+  const int bytes = colp ? (row + 1 < n ? 16 : (row < n ? 8 : 0)) : 0;
+  cp_async16(dst, bytes ? (const void*)(colp + row) : (const void*)safe, bytes);
 }
 
 // ----------------------------------------------------------------------------
-// a1: W = [Q X]^T X   (PAPER.md:L493)
+// a1: W = [Q X]^T X
 // ----------------------------------------------------------------------------
-struct GramTmaArgs {
-  StreamGeom g;                   // sx = s
+// rows per stage = kGramRB (template: 16 or 32); column stride kGramRB + 8 doubles, i.e.
+// 192 B or 320 B = 64 (mod 128): an LDS.128 phase (2 columns x 4 row pairs) touches both
+// bank halves once.
+
+struct GramCpaArgs {
+  const double* Q; int64_t ldq;
+  const double* X; int64_t ldx;
+  int64_t n; int k; int s; int NS;
   double* partials;               // [gridDim.x][m*s]
   double* W; int ldw;
   unsigned int* ticket;
 };
 
-// Each consumer warp accumulates all MT column tiles of W over its slabs
-// (acc[MTMAX][NT][2]); the 8 warps are summed in smem in fixed order at the end.
-template <int MTMAX, int NT>
-__global__ void __launch_bounds__(kStreamThreads, 1)
-    k_gram_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, GramTmaArgs a) {
-  extern __shared__ double sm_raw[];
-  const StreamGeom& g = a.g;
-  const StreamSmem S = carve(sm_raw, g);
-  const int k = g.k, s = g.sx, m = k + s, MT = (m + 7) >> 3;
+template <int MTH, int NT, int kGramRB>
+__global__ void __launch_bounds__(kCpaThreads, 2) k_gram_cpa(GramCpaArgs a) {
+  constexpr int kGramRBP = kGramRB + 8;
+  constexpr int SUBS = kGramRB / 8;           // 8-row sub-slabs per stage
+  constexpr int GROUPS = kCpaWarps / SUBS;    // column-tile groups
+  extern __shared__ __align__(16) double sm[];
+  const int k = a.k, s = a.s, m = k + s, MT = (m + 7) >> 3, mp = MT * 8;
+  const int NS = a.NS;
+  const int stage_dbl = mp * kGramRBP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, q = lane & 3;
-  stream_init(S, g, &tmQ, &tmX);
+  const int sub = warp % SUBS, half = warp / SUBS;
 
-  double acc[MTMAX][NT][2];
+  // columns m..mp-1 of every stage are never copied: zero them once
+  for (int e = tid; e < NS * (mp - m) * kGramRBP; e += kCpaThreads) {
+    const int st = e / ((mp - m) * kGramRBP), rem = e % ((mp - m) * kGramRBP);
+    sm[(size_t)st * stage_dbl + m * kGramRBP + rem] = 0.0;
+  }
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)NS * stage_dbl);
+  uint64_t* empty = full + NS;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], kCpaThreads);
+      mbar_init(&empty[i], kCpaWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t nrb = (a.n + kGramRB - 1) / kGramRB;
+  const int cnt = blockIdx.x < nrb ? (int)((nrb - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  // this thread's copy tasks (fixed across stages): chunk e = tid + 256 t -> column
+  // e / (RB/2), row pair e % (RB/2); global pointer and smem offset precomputed once
+  constexpr int RP = kGramRB / 2;
+  constexpr int TMAX = (kMMax * RP + kCpaThreads - 1) / kCpaThreads;
+  const double* tsrc[TMAX];
+  int tdst[TMAX];
+  int ntask = 0;
 #pragma unroll
-  for (int i = 0; i < MTMAX; ++i)
+  for (int t = 0; t < TMAX; ++t) {
+    const int e = tid + t * kCpaThreads;
+    const int j = e / RP, p = e % RP;
+    const bool ok = j < m;
+    tsrc[t] = ok ? col_ptr(a.Q, a.ldq, a.X, a.ldx, k, m, j) + 2 * p : a.X;
+    tdst[t] = ok ? j * kGramRBP + 2 * p : 0;
+    ntask += ok ? 1 : 0;
+  }
+  int64_t r0_p = (int64_t)blockIdx.x * kGramRB;       // producer row cursor
+  const int64_t r0_step = (int64_t)gridDim.x * kGramRB;
+  auto issue = [&](int it, int st) {
+    if (it < cnt) {
+      double* buf = sm + (size_t)st * stage_dbl;
+      if (r0_p + kGramRB <= a.n) {
+#pragma unroll
+        for (int t = 0; t < TMAX; ++t)
+          if (t < ntask) cp_async16(buf + tdst[t], tsrc[t] + r0_p, 16);
+      } else {
+#pragma unroll
+        for (int t = 0; t < TMAX; ++t)
+          if (t < ntask) {
+            const int64_t row = r0_p + ((tid + t * kCpaThreads) % RP) * 2;
+            const int bytes = row + 1 < a.n ? 16 : (row < a.n ? 8 : 0);
+            cp_async16(buf + tdst[t], bytes ? (const void*)(tsrc[t] + r0_p) : (const void*)a.X, bytes);
+          }
+      }
+      cp_async_mbar_arrive(&full[st]);
+      r0_p += r0_step;
+    }
+  };
+
+  double acc[MTH][NT][2];
+#pragma unroll
+  for (int i = 0; i < MTH; ++i)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[i][nt][0] = acc[i][nt][1] = 0.0;
 
-  const int64_t nsl = (g.n + kSlab - 1) / kSlab;
-  if (warp == kStreamConsumers) {
-    if (lane == 0) stream_produce(S, g, &tmQ, &tmX);
-  } else {
-    int j = warp;
-    for (int64_t sl = blockIdx.x + (int64_t)warp * gridDim.x; sl < nsl; sl += (int64_t)kStreamConsumers * gridDim.x,
-                 j += kStreamConsumers) {
-      const int st = j % g.NS;  // == warp + 8 * ((j / 8) % R): a stage this warp owns
-      mbar_wait(&S.full[st], (uint32_t)(j / g.NS) & 1u);
-      const double* stage = S.stages + (size_t)st * g.stage_dbl;
-      double2 bv[NT];
+  for (int it = 0; it < NS - 1; ++it) issue(it, it);
+  const int ro = sub * 8 + 2 * q;
+  int st = 0, ph = 0, stp = NS - 1;
+  // tiles past MT read the zeroed padding columns (or a valid column) and are discarded
+  int aoff[MTH];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int col = 8 * nt + gq;
-        bv[nt] = col < s ? lds2(frag_ptr(stage, k + col, k, g.k8, 2 * q)) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int mt = 0; mt < MTMAX; ++mt) {
-        if (mt < MT) {
-          const int jj = 8 * mt + gq;
-          const double2 av = jj < m ? lds2(frag_ptr(stage, jj, k, g.k8, 2 * q)) : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            dmma884(acc[mt][nt][0], acc[mt][nt][1], av.x, bv[nt].x);
-            dmma884(acc[mt][nt][0], acc[mt][nt][1], av.y, bv[nt].y);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[st]);
-    }
+  for (int i = 0; i < MTH; ++i) {
+    const int mt = half * MTH + i;
+    aoff[i] = (mt < MT ? 8 * mt + gq : 0) * kGramRBP + ro;
   }
-  __syncthreads();  // pipeline drained: stage memory is free for the reduction
-  // ---- CTA reduction over the 8 consumer warps (fixed order) ----
-  double* red = S.stages;  // [8][MT][NT][32][2]
-  const int per_warp = MT * NT * 64;
-  if (warp < kStreamConsumers) {
+  int boff[NT];
 #pragma unroll
-    for (int mt = 0; mt < MTMAX; ++mt)
-      if (mt < MT)
+  for (int nt = 0; nt < NT; ++nt) boff[nt] = (8 * nt + gq < s ? k + 8 * nt + gq : mp - 1) * kGramRBP + ro;
+  for (int it = 0; it < cnt; ++it) {
+    // stage `stp` last held item it-1: wait until every warp has released it
+    if (it >= 1) mbar_wait(&empty[stp], (uint32_t)(((it - 1) / NS) & 1));
+    issue(it + NS - 1, stp);
+    stp = stp + 1 == NS ? 0 : stp + 1;
+    mbar_wait(&full[st], (uint32_t)ph);
+    const double* buf = sm + (size_t)st * stage_dbl;
+    double2 bv[NT], av[MTH];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          red[warp * per_warp + ((mt * NT + nt) * 32 + lane) * 2 + 0] = acc[mt][nt][0];
-          red[warp * per_warp + ((mt * NT + nt) * 32 + lane) * 2 + 1] = acc[mt][nt][1];
-        }
+    for (int nt = 0; nt < NT; ++nt) bv[nt] = lds2(buf + boff[nt]);
+#pragma unroll
+    for (int i = 0; i < MTH; ++i) av[i] = lds2(buf + aoff[i]);
+#pragma unroll
+    for (int i = 0; i < MTH; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma884(acc[i][nt][0], acc[i][nt][1], av[i].x, bv[nt].x);
+#pragma unroll
+    for (int i = 0; i < MTH; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma884(acc[i][nt][0], acc[i][nt][1], av[i].y, bv[nt].y);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (++st == NS) { st = 0; ph ^= 1; }
   }
   __syncthreads();
+  // ---- CTA reduction over the SUBS sub-slab warps of each tile group (fixed order) ----
+  const int per_warp = MTH * NT * 64;
+  double* red = sm;  // [8 warps][MTH][NT][32][2]
+#pragma unroll
+  for (int i = 0; i < MTH; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      red[warp * per_warp + ((i * NT + nt) * 32 + lane) * 2 + 0] = acc[i][nt][0];
+      red[warp * per_warp + ((i * NT + nt) * 32 + lane) * 2 + 1] = acc[i][nt][1];
+    }
+  __syncthreads();
   double* part = a.partials + (size_t)blockIdx.x * m * s;
-  for (int e = tid; e < per_warp; e += blockDim.x) {
-    const int v = e & 1, l = (e >> 1) & 31, rest = e >> 6;  // rest = mt*NT + nt
-    const int nt = rest % NT, mt = rest / NT;
+  for (int e = tid; e < GROUPS * per_warp; e += kCpaThreads) {
+    const int hf = e / per_warp, r = e % per_warp;
+    const int v = r & 1, l = (r >> 1) & 31, rest = r >> 6;  // rest = i*NT + nt
+    const int nt = rest % NT, i = rest / NT;
+    const int mt = hf * MTH + i;
     const int jj = 8 * mt + (l >> 2), c = 8 * nt + 2 * (l & 3) + v;
-    if (jj < m && c < s) {
+    if (mt < MT && jj < m && c < s) {
       double sum = 0.0;
-      for (int w = 0; w < kStreamConsumers; ++w) sum += red[w * per_warp + e];
+      for (int sb = 0; sb < SUBS; ++sb) sum += red[(hf * SUBS + sb) * per_warp + r];
       part[jj + (int64_t)c * m] = sum;
     }
   }
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   __threadfence();
   const int ms = m * s;
   const int nb = gridDim.x;
-  for (int e = tid; e < ms; e += blockDim.x) {
+  for (int e = tid; e < ms; e += kCpaThreads) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int b = 0;
     for (; b + 4 <= nb; b += 4) {
@@ -219,98 +221,159 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
 }
 
 // ----------------------------------------------------------------------------
-// a4: U = [Q X] M   ("U = XN^{-1} - QPN^{-1}")
+// a4: U = [Q X] M
 // ----------------------------------------------------------------------------
-struct UpdTmaArgs {
-  StreamGeom g;
-  int sout;
+constexpr int kUpdRB = 128;   // rows per row block (8 warps x 16)
+constexpr int kUpdRBP = 132;  // column stride (doubles): 1056 B = 32 (mod 128) -> an LDS.128
+                              // phase (4 columns x 2 row pairs) hits 4 disjoint bank octets
+
+struct UpdCpaArgs {
+  const double* Q; int64_t ldq;
+  const double* X; int64_t ldx;
+  int64_t n; int k; int sx; int sout;
   const double* M; int ldm;       // (k+sx) x sout
   const int* t_dev;
   double* U; int64_t ldu;
   double* U2; int64_t ldu2;
+  int NS;
 };
 
-// U^T = M^T [Q X]^T as m8n8k4 MMAs: M-index = output column c, N-index = slab row,
-// K = column j of [Q X].  Lane l reads row l>>2 of column 4kk+(l&3) (B fragment) and
-// M[4kk+(l&3)][l>>2] (A fragment); the D fragment gives it rows 2(l&3), 2(l&3)+1 of
-// output column l>>2.  Two accumulator chains (even / odd kk) halve the DMMA
-// dependency chain.
-template <int NT>
-PQR_DEV void upd_store_pair(const UpdTmaArgs& a, const double (&d)[NT][2], int64_t row, int gq, int t) {
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int c = 8 * nt + gq;
-    if (c >= a.sout) continue;
-    const bool valid = c < t;
-    const double v0 = valid ? d[nt][0] : 0.0, v1 = valid ? d[nt][1] : 0.0;
-    double* up = a.U + (int64_t)c * a.ldu + row;
-    if (row + 1 < a.g.n) st2(up, v0, v1);
-    else if (row < a.g.n) up[0] = v0;
-    if (a.U2 && valid) {
-      double* u2 = a.U2 + (int64_t)c * a.ldu2 + row;
-      if (row + 1 < a.g.n) st2(u2, v0, v1);
-      else if (row < a.g.n) u2[0] = v0;
-    }
-  }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(kStreamThreads, 1)
-    k_update_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, UpdTmaArgs a) {
-  extern __shared__ double sm_raw[];
-  const StreamGeom& g = a.g;
-  const StreamSmem S = carve(sm_raw, g);
-  const int k = g.k, m = k + g.sx;
-  const int KS = ((m + 7) >> 3) * 2, mpad = KS * 4;  // even number of k-steps
-  double* sM = reinterpret_cast<double*>(S.empty + g.NS);  // [NT][mpad][8]
+// U^T = M^T [Q X]^T as m8n8k4 MMAs: M-index = output column c, N-index = row, K = column j
+// of [Q X].  Lane l reads rows 2(l>>2), 2(l>>2)+1 of column 4kk+(l&3): the even row feeds
+// one MMA, the odd row another; the D fragments give each lane 4 consecutive rows.
+template <int NT, int kUpdCW>
+__global__ void __launch_bounds__(kCpaThreads, 2) k_update_cpa(UpdCpaArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int k = a.k, m = k + a.sx;
+  const int NCH = (m + kUpdCW - 1) / kUpdCW, mpad = NCH * kUpdCW;
+  const int NS = a.NS;
+  constexpr int stage_dbl = kUpdCW * kUpdRBP;
+  double* sM = sm;                                  // [NT][mpad][8]
+  double* stages = sm + (size_t)NT * mpad * 8;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, q = lane & 3;
-  for (int e = tid; e < NT * mpad * 8; e += blockDim.x) {
+  for (int e = tid; e < NT * mpad * 8; e += kCpaThreads) {
     const int nt = e / (mpad * 8), rem = e % (mpad * 8);
     const int j = rem >> 3, c = 8 * nt + (rem & 7);
     sM[e] = (j < m && c < a.sout) ? a.M[j + (int64_t)c * a.ldm] : 0.0;
   }
-  stream_init(S, g, &tmQ, &tmX);
-  const int t = a.t_dev ? *a.t_dev : a.sout;
-  const int64_t nsl = (g.n + kSlab - 1) / kSlab;
-
-  if (warp == kStreamConsumers) {
-    if (lane == 0) stream_produce(S, g, &tmQ, &tmX);
-    return;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)NS * stage_dbl);
+  uint64_t* empty = full + NS;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], kCpaThreads);
+      mbar_init(&empty[i], kCpaWarps);
+    }
+    fence_mbar_init();
   }
-  int j = warp;
-  for (int64_t sl = blockIdx.x + (int64_t)warp * gridDim.x; sl < nsl; sl += (int64_t)kStreamConsumers * gridDim.x,
-               j += kStreamConsumers) {
-    const int st = j % g.NS;
-    mbar_wait(&S.full[st], (uint32_t)(j / g.NS) & 1u);
-    const double* stage = S.stages + (size_t)st * g.stage_dbl;
-    double d[2][NT][2];
+  const int t = a.t_dev ? *a.t_dev : a.sout;
+  const int64_t nrb = (a.n + kUpdRB - 1) / kUpdRB;
+  const int cnt_rb = blockIdx.x < nrb ? (int)((nrb - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int cnt = cnt_rb * NCH;
+  const double* safe = a.k > 0 ? a.Q : a.X;
+  // producer cursor (item = (row block, chunk)); this thread's 4 chunks per stage:
+  // e = tid + 256 t -> column (e >> 6) of the chunk, row pair e & 63
+  constexpr int TU = kUpdCW * (kUpdRB / 2) / kCpaThreads;
+  int ch_p = 0;
+  int64_t r0_p = (int64_t)blockIdx.x * kUpdRB;
+  const int64_t r0_step = (int64_t)gridDim.x * kUpdRB;
+  auto issue = [&](int it, int st) {
+    if (it < cnt) {
+      double* buf = stages + (size_t)st * stage_dbl;
+      const int j0 = ch_p * kUpdCW;
+      const bool full_rows = r0_p + kUpdRB <= a.n;
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+      for (int t = 0; t < TU; ++t) {
+        const int e = tid + t * kCpaThreads;
+        const int jl = e >> 6, p = e & 63;
+        const double* cp = col_ptr(a.Q, a.ldq, a.X, a.ldx, k, m, j0 + jl);
+        const int64_t row = r0_p + 2 * p;
+        const int bytes = !cp ? 0 : (full_rows || row + 1 < a.n ? 16 : (row < a.n ? 8 : 0));
+        cp_async16(buf + jl * kUpdRBP + 2 * p, bytes ? (const void*)(cp + row) : (const void*)safe, bytes);
+      }
+      cp_async_mbar_arrive(&full[st]);
+      if (++ch_p == NCH) {
+        ch_p = 0;
+        r0_p += r0_step;
+      }
+    }
+  };
+  __syncthreads();  // sM and barriers ready
+  for (int it = 0; it < NS - 1; ++it) issue(it, it);
+  double d[NT][2][2], e2[NT][2][2];  // two accumulator sets (even / odd k-steps) for ILP
+  const int so = 16 * warp + 2 * gq;
+  int st = 0, ph = 0, stp = NS - 1, ch = 0;
+  int64_t r0 = (int64_t)blockIdx.x * kUpdRB;
+  for (int it = 0; it < cnt; ++it) {
+    if (ch == 0) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) d[h][nt][0] = d[h][nt][1] = 0.0;
-#pragma unroll 4
-    for (int kk = 0; kk < KS; kk += 2) {
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = 4 * (kk + h) + q;
-        const double bv = jj < m ? *frag_ptr(stage, jj, k, g.k8, gq) : 0.0;
+        for (int x = 0; x < 2; ++x) d[nt][x][0] = d[nt][x][1] = e2[nt][x][0] = e2[nt][x][1] = 0.0;
+    }
+    if (it >= 1) mbar_wait(&empty[stp], (uint32_t)(((it - 1) / NS) & 1));
+    issue(it + NS - 1, stp);
+    stp = stp + 1 == NS ? 0 : stp + 1;
+    mbar_wait(&full[st], (uint32_t)ph);
+    const double* buf = stages + (size_t)st * stage_dbl;
+    const double* mrow = sM + (ch * kUpdCW) * 8 + gq;
+    double2 av[kUpdCW / 4];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const double mv = sM[(nt * mpad + jj) * 8 + gq];
-          dmma884(d[h][nt][0], d[h][nt][1], mv, bv);
-        }
+    for (int kk = 0; kk < kUpdCW / 4; ++kk) av[kk] = lds2(buf + (4 * kk + q) * kUpdRBP + so);
+#pragma unroll
+    for (int kk = 0; kk < kUpdCW / 4; ++kk) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double mv = mrow[(nt * mpad + 4 * kk + q) * 8];
+        double (&acc)[2][2] = (kk & 1) ? e2[nt] : d[nt];
+        dmma884(acc[0][0], acc[0][1], mv, av[kk].x);
+        dmma884(acc[1][0], acc[1][1], mv, av[kk].y);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[st]);
-    double r[NT][2];
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (++st == NS) { st = 0; ph ^= 1; }
+    if (++ch == NCH) {
+      ch = 0;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      r[nt][0] = d[0][nt][0] + d[1][nt][0];
-      r[nt][1] = d[0][nt][1] + d[1][nt][1];
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          d[nt][x][0] += e2[nt][x][0];
+          d[nt][x][1] += e2[nt][x][1];
+        }
+      const int64_t row = r0 + 16 * warp + 4 * q;
+      r0 += (int64_t)gridDim.x * kUpdRB;
+      const bool full_rows = row + 3 < a.n;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c = 8 * nt + gq;
+        if (c >= a.sout) continue;
+        const bool valid = c < t;
+        const double v0 = valid ? d[nt][0][0] : 0.0, v1 = valid ? d[nt][1][0] : 0.0;
+        const double v2 = valid ? d[nt][0][1] : 0.0, v3 = valid ? d[nt][1][1] : 0.0;
+        double* up = a.U + (int64_t)c * a.ldu + row;
+        if (full_rows) {
+          st2(up, v0, v1);
+          st2(up + 2, v2, v3);
+        } else {
+          if (row + 0 < a.n) up[0] = v0;
+          if (row + 1 < a.n) up[1] = v1;
+          if (row + 2 < a.n) up[2] = v2;
+        }
+        if (a.U2 && valid) {
+          double* u2 = a.U2 + (int64_t)c * a.ldu2 + row;
+          if (full_rows) {
+            st2(u2, v0, v1);
+            st2(u2 + 2, v2, v3);
+          } else {
+            if (row + 0 < a.n) u2[0] = v0;
+            if (row + 1 < a.n) u2[1] = v1;
+            if (row + 2 < a.n) u2[2] = v2;
+          }
+        }
+      }
     }
-    upd_store_pair<NT>(a, r, sl * kSlab + 2 * q, gq, t);
   }
 }
 
