@@ -14,6 +14,7 @@
 #include "../../include/pqr_steps.h"
 #include "cholqr_kernels.cuh"
 #include "tsqr_kernels.cuh"
+#include "tsqr_wy.cuh"
 #include "stream_kernels.cuh"
 
 using namespace pqr;

@@ -1,0 +1,461 @@
+// tsqr_wy.cuh — TreeTSPQR level kernels with blocked (compact-WY) reflector panels and
+// fp64 MMAs (§4.1 Alg. 9 with Householder local/reduction subalgorithms).
+//
+// A level block holds R <= 256*UW rows; warp w (of 16) owns UW units of 16
+// rows, lane (g = l>>2, q = l&3) keeping rows 16u+4q+{0..3} of columns 8nt+g in
+// registers (the D-fragment layout of the update MMA below).  The block's reflectors
+// are grouped in panels (the reflectors created by one call, or one LOR-build chunk):
+// H_a ... H_b = I - V T V^T with T^{-1} = I/2 + striu(V^T V) (unit-norm v, Eq. (hh)).
+//
+//   stage 1 (Q_b^T X):  for each panel in order   Z = V^T X, Z' = T^T Z, X -= V Z'
+//   stage 2 (Q_b Y):    for each panel reversed    Z = V^T Y, Z' = T Z,   Y -= V Z'
+//
+// Z = V^T X is an m8n8k4 DMMA Gram (K = rows: lane q supplies rows 4q..4q+3 as four
+// k-steps); X -= V Z' is X^T -= Z'^T V^T (K = panel columns, N = rows, the even/odd
+// row trick of the update kernel).  Panels are double-buffered in shared memory with
+// cp.async; the panel stride RP = 10 (mod 16) doubles makes both fragment patterns
+// bank-conflict-free (the update k-steps take columns 2q+kk so the four columns of an
+// LDS.128 phase land in four distinct 32-byte bank groups).
+//
+// After the committed panels, stage 1 factors rows C..R-1 of the s new columns with
+// Householder reflectors (Alg. 6 lines 2-9; never deflating, reading R4), stores them
+// (rows < pivot zeroed) and the panel's T, and writes [P_b; N_b] to the parent slot.
+#pragma once
+#include "common.cuh"
+
+namespace pqr {
+
+constexpr int kWyWarps = 16;
+constexpr int kWyThreads = 32 * kWyWarps;
+constexpr int kWyRowsPerUW = 16 * kWyWarps;  // block rows covered per unit-per-warp
+constexpr int kWyMaxW = 16;  // widest panel
+
+struct WyLevel {
+  int64_t q, rem2;      // block b: q + 2*(b < rem2) rows starting at b*q + 2*min(b, rem2) (even);
+  int odd_last;         // ... the last block has one more row when the level's row count is odd
+  int nblocks;
+  const double* X; int64_t ldx;     // stage-1 input (level rows)
+  double* V; int64_t ldv;           // reflectors (level rows); column j = reflector j
+  double* T; int64_t tstride;       // block b's T area at T + b*tstride; panel at +16*start
+  double* out; int64_t ldo;         // stage-1 output: block b -> rows b*cap ...
+  const double* cin; int64_t ldci;  // stage-2 coefficients: block b -> rows b*cap ...
+  double* Y; int64_t ldy;           // stage-2 output (level rows)
+  int cap;
+  int RP;                           // smem panel stride (>= max block rows, = 10 mod 16)
+  int wmax;                         // widest panel (<= 16) -> smem panel buffer width
+};
+
+struct WyPanels {
+  const int2* pan;  // (start, width) per panel, device
+  int np;           // panels to apply
+};
+
+PQR_DEV int64_t wy_start(const WyLevel& L, int64_t b) { return b * L.q + 2 * (b < L.rem2 ? b : L.rem2); }
+PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
+  return (int)(L.q + (b < L.rem2 ? 2 : 0) + (b == L.nblocks - 1 ? L.odd_last : 0));
+}
+
+// column of the update k-step kk for lane quarter q (conflict-free pattern, see header)
+PQR_DEV int wy_col(int kk, int q) { return 8 * (kk >> 1) + 2 * q + (kk & 1); }
+
+// Stage panel (start, w) of this block into buf (RP x w8 col-major); rows R..kWyRowsPerUW*UW-1
+// and columns w..w8-1 are zero-filled (they meet zero rows / zero coefficients in the MMAs).
+template <int UW>
+PQR_DEV void wy_load_panel(double* buf, const WyLevel& L, int64_t r0, int R, int start, int w, int RP) {
+  constexpr int pairs = kWyRowsPerUW * UW / 2;
+  const int w8 = (w + 7) & ~7;
+  for (int e = threadIdx.x; e < w8 * pairs; e += kWyThreads) {
+    const int j = e / pairs, p = e - j * pairs;
+    const int row = 2 * p;
+    const double* src = L.V + (int64_t)(start + j) * L.ldv + r0 + row;
+    const int bytes = (j < w && row < R) ? (row + 1 < R ? 16 : 8) : 0;
+    cp_async16(buf + j * RP + row, bytes ? (const void*)src : (const void*)L.V, bytes);
+  }
+}
+
+// Block-wide: Z (w8 x s8, smem, col-major ld 16) = sum over warps of the D fragments
+// acc[mt][nt][2]; red is kWyWarps*256 doubles.  Ends with a __syncthreads.
+template <int NT>
+PQR_DEV void wy_reduce_Z(double (&acc)[2][NT][2], int mtn, double* red, double* Z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = 8 * mt + g, c = 8 * nt + 2 * q + v;
+        red[warp * 256 + i + 16 * c] = (mt < mtn) ? acc[mt][nt][v] : 0.0;
+      }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 256; e += kWyThreads) {
+    double a = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWyWarps; ++w) a += red[w * 256 + e];
+    Z[e] = a;
+  }
+  __syncthreads();
+}
+
+// apply one panel (in smem `vb`, width w) to the register block x:
+//   x <- x - V (Tp Z),  Z = V^T x,  Tp = T^T (stage 1) or T (stage 2);  Tg in smem (ld w)
+template <int UW, int NT>
+PQR_DEV void wy_apply_panel(double (&x)[UW][NT][4], const double* vb, const double* Tg, int w, bool transT,
+                            int RP, double* red, double* Zp) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int mtn = (w + 7) >> 3;
+  // ---- Z = V^T x (per-warp partials; two accumulator chains over alternate units) ----
+  double acc[2][2][NT][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    if (mt < mtn) {
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        const int row = 16 * (warp * UW + u) + 4 * q;
+        const double* vp = vb + (8 * mt + g) * RP + row;
+        const double2 a01 = *reinterpret_cast<const double2*>(vp);
+        const double2 a23 = *reinterpret_cast<const double2*>(vp + 2);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double (&ac)[2] = acc[u & 1][mt][nt];
+          dmma884(ac[0], ac[1], a01.x, x[u][nt][0]);
+          dmma884(ac[0], ac[1], a01.y, x[u][nt][1]);
+          dmma884(ac[0], ac[1], a23.x, x[u][nt][2]);
+          dmma884(ac[0], ac[1], a23.y, x[u][nt][3]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int i = 8 * mt + g, c = 8 * nt + 2 * q + v;
+        red[warp * 256 + i + 16 * c] = (mt < mtn) ? acc[0][mt][nt][v] + acc[1][mt][nt][v] : 0.0;
+      }
+  __syncthreads();
+  // ---- Z' = T^T Z (stage 1) or T Z (stage 2), Z = sum over warps of red ----
+  for (int e = tid; e < 256; e += kWyThreads) {
+    const int i = e & 15, c = e >> 4;
+    double a = 0.0;
+    if (i < w) {
+      const int l0 = transT ? 0 : i, l1 = transT ? i : w - 1;
+      for (int l = l0; l <= l1; ++l) {
+        double z = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < kWyWarps; ++ww) z += red[ww * 256 + l + 16 * c];
+        a += (transT ? Tg[l + i * w] : Tg[i + l * w]) * z;
+      }
+    }
+    Zp[e] = a;
+  }
+  __syncthreads();
+  // ---- x^T -= Z'^T V^T ----
+  const int kks = 2 * mtn;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    if (kk < kks) {
+      const int j = wy_col(kk, q);
+      double am[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) am[nt] = -Zp[j + 16 * (8 * nt + g)];
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        const int row = 16 * (warp * UW + u) + 2 * g;
+        const double2 bv = *reinterpret_cast<const double2*>(vb + j * RP + row);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma884(x[u][nt][0], x[u][nt][2], am[nt], bv.x);  // even rows 4q, 4q+2
+          dmma884(x[u][nt][1], x[u][nt][3], am[nt], bv.y);  // odd rows 4q+1, 4q+3
+        }
+      }
+    }
+  }
+}
+
+// Apply the first np panels, forward (stage 1, H_0 first, T^T) or reversed (stage 2, T).
+// The panel list and this block's T factors are staged in shared memory (Ts, 16*cap
+// doubles; pans, np entries); panels are double-buffered with cp.async.
+template <int UW, int NT>
+PQR_DEV void wy_apply_panels(double (&x)[UW][NT][4], const WyLevel& L, const WyPanels& P, int64_t b, int64_t r0,
+                             int R, bool forward, double* vbuf, double* red, double* Zp, double* Ts, int2* pans) {
+  const int np = P.np;
+  if (np == 0) return;
+  const int RP = L.RP;
+  const int pstride = RP * L.wmax;
+  for (int i = threadIdx.x; i < np; i += kWyThreads) pans[i] = P.pan[i];
+  const double* Tb = L.T + b * L.tstride;
+  __syncthreads();
+  const int2 last = pans[np - 1];
+  const int tlen = 16 * last.x + last.y * last.y;  // T area used by the panels
+  for (int e = threadIdx.x; e < tlen; e += kWyThreads) Ts[e] = Tb[e];
+  auto pidx = [&](int i) { return forward ? i : np - 1 - i; };
+  {
+    const int2 pn = pans[pidx(0)];
+    wy_load_panel<UW>(vbuf, L, r0, R, pn.x, pn.y, RP);
+    cp_async_commit();
+  }
+  for (int i = 0; i < np; ++i) {
+    if (i + 1 < np) {
+      const int2 pn = pans[pidx(i + 1)];
+      wy_load_panel<UW>(vbuf + ((i + 1) & 1) * pstride, L, r0, R, pn.x, pn.y, RP);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const int2 pc = pans[pidx(i)];
+    wy_apply_panel<UW, NT>(x, vbuf + (i & 1) * pstride, Ts + 16 * pc.x, pc.y, forward, RP, red, Zp);
+    __syncthreads();  // the buffer is refilled two iterations later
+  }
+  cp_async_wait<0>();
+}
+
+// ----------------------------------------------------------------------------
+// stage 1
+// ----------------------------------------------------------------------------
+template <int UW, int NT>
+__global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s) {
+  extern __shared__ __align__(16) double sm[];
+  const int RP = L.RP;
+  double* vbuf = sm;                                   // 2 x RP x wmax
+  double* red = vbuf + 2 * RP * L.wmax;                // 8 x 256
+  double* Z = red + kWyWarps * 256;                    // 256
+  double* Zp = Z + 256;                                // 256
+  double* bc = Zp + 256;                               // 64 scratch
+  double* Ts = bc + 64;                                // 16 * cap: this block's T factors
+  int2* pans = reinterpret_cast<int2*>(Ts + 16 * L.cap);  // panel list
+  double* Vn = vbuf;                                   // RP x s8: the new reflectors (aliases the
+                                                       // panel buffers, free after the panels)
+  const int64_t b = blockIdx.x;
+  const int64_t r0 = wy_start(L, b);
+  const int R = wy_rows(L, b);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+
+  double x[UW][NT][4];
+#pragma unroll
+  for (int u = 0; u < UW; ++u)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+        x[u][nt][i] = (row < R && c < s) ? L.X[r0 + row + (int64_t)c * L.ldx] : 0.0;
+      }
+  wy_apply_panels<UW, NT>(x, L, P, b, r0, R, true, vbuf, red, Zp, Ts, pans);
+
+  // ---- Householder QR of rows C..R-1 of the s new columns ----
+  __syncthreads();
+  for (int e = tid; e < RP * ((s + 7) & ~7); e += kWyThreads) Vn[e] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < s; ++c) {
+    const int r = C + c;
+    const int ntc = c >> 3, gc = c & 7;
+    // lambda^2 over rows >= r of column c, and u0 = x[r][c]
+    double part = 0.0;
+    if (g == gc) {
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          if (nt == ntc)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int row = 16 * (warp * UW + u) + 4 * q + i;
+              if (row >= r && row < R) part += x[u][nt][i] * x[u][nt][i];
+              if (row == r) bc[0] = x[u][nt][i];
+            }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    double lam2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWyWarps; ++w) lam2 += red[w];
+    const double lam = sqrt(lam2);
+    const double u0 = bc[0];
+    const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
+    const double diag = sigma * lam;
+    const double nv2 = 2.0 * lam * (lam + fabs(u0));
+    const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lam == 0 (R4)
+    // v on this lane's rows (valid in lanes g == gc); column c becomes [x(0:r); diag; 0]
+    double vv[UW][4];
+#pragma unroll
+    for (int u = 0; u < UW; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 16 * (warp * UW + u) + 4 * q + i;
+        double xv = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          if (nt == ntc) xv = x[u][nt][i];
+        const double v = (row > r && row < R) ? xv * inv : (row == r ? (xv - diag) * inv : 0.0);
+        vv[u][i] = v;
+        if (g == gc) {
+          if (row < R) Vn[c * RP + row] = v;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            if (nt == ntc && row >= r) x[u][nt][i] = (row == r) ? diag : 0.0;
+        }
+      }
+    // apply H = I - 2 v v^T to columns c+1..s-1: lanes of column c' fetch v from lane (gc, q)
+    if (c + 1 < s) {
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vv[u][i] = __shfl_sync(0xffffffffu, vv[u][i], gc * 4 + q);
+      double dp[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double a = 0.0;
+        if (8 * nt + g > c) {
+#pragma unroll
+          for (int u = 0; u < UW; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a += vv[u][i] * x[u][nt][i];
+        }
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        dp[nt] = a;
+      }
+      __syncthreads();  // red[] reads of the norm step are done
+      if (q == 0) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) red[warp * 16 + 8 * nt + g] = dp[nt];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int cc = 8 * nt + g;
+        if (cc > c && cc < s) {
+          double d = 0.0;
+#pragma unroll
+          for (int w = 0; w < kWyWarps; ++w) d += red[w * 16 + cc];
+          const double f = 2.0 * d;
+#pragma unroll
+          for (int u = 0; u < UW; ++u)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[u][nt][i] -= f * vv[u][i];
+        }
+      }
+    }
+    __syncthreads();  // red / bc reuse
+  }
+
+  // ---- outputs: [P_b; N_b] = rows 0..C+s-1, the new reflectors, the new panel's T ----
+  double* outb = L.out + b * L.cap;
+#pragma unroll
+  for (int u = 0; u < UW; ++u)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+        if (row < C + s && row < R && c < s) outb[row + (int64_t)c * L.ldo] = x[u][nt][i];
+      }
+  for (int e = tid; e < s * R; e += kWyThreads) {
+    const int c = e / R, row = e - c * R;
+    L.V[r0 + row + (int64_t)(C + c) * L.ldv] = Vn[c * RP + row];
+  }
+  // V^T V of the new panel: Gram MMA from smem Vn (same fragment pattern as Z = V^T x)
+  {
+    double acc[2][2][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const int mtn = (s + 7) >> 3;
+#pragma unroll
+    for (int u = 0; u < UW; ++u) {
+      const int row = 16 * (warp * UW + u) + 4 * q;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        if (nt < mtn) {
+          const double2 b01 = *reinterpret_cast<const double2*>(Vn + (8 * nt + g) * RP + row);
+          const double2 b23 = *reinterpret_cast<const double2*>(Vn + (8 * nt + g) * RP + row + 2);
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            if (mt < mtn) {
+              const double2 a01 = *reinterpret_cast<const double2*>(Vn + (8 * mt + g) * RP + row);
+              const double2 a23 = *reinterpret_cast<const double2*>(Vn + (8 * mt + g) * RP + row + 2);
+              dmma884(acc[mt][nt][0], acc[mt][nt][1], a01.x, b01.x);
+              dmma884(acc[mt][nt][0], acc[mt][nt][1], a01.y, b01.y);
+              dmma884(acc[mt][nt][0], acc[mt][nt][1], a23.x, b23.x);
+              dmma884(acc[mt][nt][0], acc[mt][nt][1], a23.y, b23.y);
+            }
+          }
+        }
+      }
+    }
+    wy_reduce_Z<2>(acc, mtn, red, Z);  // Z = V^T V (16 x 16, ld 16)
+    // T^{-1} = I/2 + striu(V^T V);  T = its inverse (upper triangular), column c by lane c
+    double* Tn = L.T + b * L.tstride + 16 * C;
+    if (tid < s) {
+      const int c = tid;
+      double col[kWyMaxW];
+#pragma unroll
+      for (int i = 0; i < kWyMaxW; ++i) col[i] = 0.0;
+      col[c] = 2.0;  // 1 / (1/2)
+      for (int i = c - 1; i >= 0; --i) {
+        double a = 0.0;
+        for (int l = i + 1; l <= c; ++l) a += Z[i + 16 * l] * col[l];
+        col[i] = -a * 2.0;
+      }
+      for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// stage 2: Y_b = Q_b [coef; 0]
+// ----------------------------------------------------------------------------
+template <int UW, int NT>
+__global__ void __launch_bounds__(kWyThreads, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
+  extern __shared__ __align__(16) double sm[];
+  const int RP = L.RP;
+  double* vbuf = sm;
+  double* red = vbuf + 2 * RP * L.wmax;
+  double* Z = red + kWyWarps * 256;
+  double* Zp = Z + 256;
+  double* Ts = Zp + 256 + 64;
+  int2* pans = reinterpret_cast<int2*>(Ts + 16 * L.cap);
+  const int64_t b = blockIdx.x;
+  const int64_t r0 = wy_start(L, b);
+  const int R = wy_rows(L, b);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const double* cb = L.cin + b * L.cap;
+  double y[UW][NT][4];
+#pragma unroll
+  for (int u = 0; u < UW; ++u)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+        y[u][nt][i] = (row < Call && row < R && c < t) ? cb[row + (int64_t)c * L.ldci] : 0.0;
+      }
+  wy_apply_panels<UW, NT>(y, L, P, b, r0, R, false, vbuf, red, Zp, Ts, pans);
+#pragma unroll
+  for (int u = 0; u < UW; ++u)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+        if (row < R && c < ncol) L.Y[r0 + row + (int64_t)c * L.ldy] = c < t ? y[u][nt][i] : 0.0;
+      }
+}
+
+}  // namespace pqr
