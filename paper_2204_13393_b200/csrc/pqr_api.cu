@@ -12,10 +12,12 @@
 
 #include "../../include/pqr.h"
 #include "../../include/pqr_steps.h"
+#include "../../include/pqr_support.h"
 #include "cholqr_kernels.cuh"
 #include "tsqr_kernels.cuh"
 #include "tsqr_wy.cuh"
 #include "stream_kernels.cuh"
+#include "support_kernels.cuh"
 
 using namespace pqr;
 
@@ -720,6 +722,19 @@ int pqr_nccl_unique_id(void* id128) {
 // ---------------------------------------------------------------------------
 // step-level entry points (include/pqr_steps.h)
 // ---------------------------------------------------------------------------
+int pqr_laplacian7_apply(int nx, int ny, int nz, int s, const double* V, int64_t ldv, double* Y, int64_t ldy,
+                         void* stream) {
+  const int64_t npts = (int64_t)nx * ny * nz;
+  if (nx < 1 || ny < 1 || nz < 1 || s < 1 || s > 16 || !V || !Y || ldv < npts || ldy < npts) return PQR_EARG;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t work = npts * s;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 16, (work + 255) / 256));
+  k_laplacian7<<<grid, 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, s, V, ldv, Y, ldy);
+  return cudaGetLastError() == cudaSuccess ? PQR_OK : PQR_ECUDA;
+}
+
 int pqr_step_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double* X, int64_t ldx, double* W,
                   int ldw, void* stream) {
   if (n <= 0 || k < 0 || s < 1 || s > kSMax || k + s > kMMax || !X || ldx < n || (k > 0 && (!Q || ldq < n)) ||

@@ -54,7 +54,7 @@ PROFILE_KINDS = ["gram", "factor", "update", "nccl", "tsqr_local", "tsqr_tree", 
 
 EXPORTS = ["pqr_create", "pqr_project_normalize", "pqr_basis_apply", "pqr_destroy", "pqr_strerror",
            "pqr_get_stats", "pqr_profile_enable", "pqr_get_profile", "pqr_nccl_unique_id",
-           "pqr_step_gram", "pqr_step_factor", "pqr_step_update"]
+           "pqr_step_gram", "pqr_step_factor", "pqr_step_update", "pqr_laplacian7_apply"]
 
 _lib = None
 
@@ -82,6 +82,7 @@ def lib():
     L.pqr_step_factor.argtypes = [i, i, vp, i, d, d, vp, i, vp, i, ctypes.POINTER(ctypes.c_int),
                                   ctypes.POINTER(ctypes.c_int), vp]
     L.pqr_step_update.argtypes = [i64, i, i, vp, i64, vp, i64, vp, i, i, vp, i64, vp]
+    L.pqr_laplacian7_apply.argtypes = [i, i, i, i, vp, i64, vp, i64, vp]
     for f in EXPORTS:
         if f != "pqr_strerror":
             getattr(L, f).restype = ctypes.c_int
@@ -241,6 +242,13 @@ def pqr_step_update(n, k, s, Q, X, M, t, U, stream=None):
     up, ldu = _mat(U)
     _check(lib().pqr_step_update(int(n), int(k), int(s), qp, ldq, xp, ldx, mp, ldm, int(t), up, ldu,
                                  _stream_ptr(stream)), "pqr_step_update")
+
+
+def pqr_laplacian7_apply(nx, ny, nz, s, V, Y, stream=None):
+    vp, ldv = _mat(V)
+    yp, ldy = _mat(Y)
+    _check(lib().pqr_laplacian7_apply(int(nx), int(ny), int(nz), int(s), vp, ldv, yp, ldy, _stream_ptr(stream)),
+           "pqr_laplacian7_apply")
 
 
 # ---------------------------------------------------------------------------

@@ -34,7 +34,12 @@ def ortho_loss_2(Q, U):
     """||I - [Q U]^T [Q U]||_2 on the device (torch fp64 GEMM; test-side check only)."""
     import torch
 
-    A = torch.cat([Q, U], dim=1) if Q.shape[1] else U
-    G = A.t() @ A
-    G -= torch.eye(G.shape[0], dtype=G.dtype, device=G.device)
+    k, t = Q.shape[1], U.shape[1]
+    G = torch.empty((k + t, k + t), dtype=torch.float64, device=U.device)
+    if k:
+        G[:k, :k] = Q.t() @ Q
+        G[:k, k:] = Q.t() @ U
+        G[k:, :k] = G[:k, k:].t()
+    G[k:, k:] = U.t() @ U
+    G -= torch.eye(k + t, dtype=G.dtype, device=G.device)
     return float(torch.linalg.matrix_norm(G, ord=2))
