@@ -5,8 +5,10 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload weak|single|deflation|tiny]
                   [--variant cholqr2|tsqr|both] [--impl pqr|reference]
 
-One step = one pqr_project_normalize call per selected variant (PQR_NO_APPEND, so the
-basis and all inputs are identical every step) over the workload's synthetic block.
+One step = one pqr_project_normalize call per selected variant (default: both, so a step
+covers every row of SURVEY.md §8(a): CholQR2 a1-a5 and TSQR a6-a8) with PQR_NO_APPEND, so
+the basis and all inputs are identical every step.  --workload arnoldi instead times the
+32 PQR calls of one block-Arnoldi run (configs[2]; the stencil is timed separately).
 Default workload = configs[4] ("weak": 2^25 rows per GPU, k=128, s=8), the config the
 metric is quoted on at 1/2/4/8 GPUs; per-GPU work is fixed, so scaling is "weak".
 
@@ -32,6 +34,7 @@ sys.path.insert(0, ROOT)
 SEED = 2204133930
 WORKLOADS = {
     "tiny": dict(n=10_000, k=32, s=4, cfg_index=0),
+    "arnoldi": dict(n=256 ** 3, k=128, s=4, grid=256, steps=32, cfg_index=2),
     "single": dict(n=2 ** 24, k=64, s=8, cfg_index=1),
     "deflation": dict(n=2 ** 22, k=96, s=16, cfg_index=3),
     "weak": dict(n=2 ** 25, k=128, s=8, cfg_index=4),
@@ -191,7 +194,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="weak", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="cholqr2", choices=["cholqr2", "tsqr", "both"])
+    ap.add_argument("--variant", default="both", choices=["cholqr2", "tsqr", "both"])
     ap.add_argument("--impl", default="pqr", choices=["pqr", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -217,6 +220,8 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=device)
+    if args.workload == "arnoldi":
+        return run_arnoldi(args, rank, world, local_rank, device)
     w = WORKLOADS[args.workload]
     n, k, s = w["n"], w["k"], w["s"]
     stream = torch.cuda.current_stream(device)
@@ -238,11 +243,9 @@ def main():
     Nm = inputs.colmajor_empty(s, s, device)
     torch.cuda.synchronize()
 
-    nccl_id = None
-    if world > 1:
-        obj = [pqr.pqr_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    from paper_2204_13393_b200 import dist as pdist
+
+    nccl_id = pdist.nccl_id_for_library(world)
 
     variants = ["cholqr2", "tsqr"] if args.variant == "both" else [args.variant]
     handles = {}
@@ -251,10 +254,21 @@ def main():
     del Q
     torch.cuda.empty_cache()
 
+    var_ms = {v: 0.0 for v in variants}
+    timing = {"on": False}
+
     def step():
         ts = []
         for v in variants:
+            if timing["on"]:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
             ts.append(handles[v].solve(X, U=U, P=Pm, N=Nm, flags=pqr.PQR_NO_APPEND))
+            if timing["on"]:
+                b.record(stream)
+                b.synchronize()
+                var_ms[v] += a.elapsed_time(b)
         return ts
 
     def barrier():
@@ -270,6 +284,7 @@ def main():
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    timing["on"] = True
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -372,11 +387,91 @@ def main():
             "frac_of_roofline": frac_whole,
             "roofline": roof,
             "kernel_share": share,
+            "variant_ms_per_call": {v: var_ms[v] / args.steps for v in variants},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_arnoldi(args, rank, world, local_rank, device):
+    """configs[2]: block Arnoldi on the 256^3 7-point Laplacian, s = 4, 32 PQR calls with
+    k = 4..128 (after the k = 0 start).  Each rank runs its own replica (the Arnoldi operator
+    is not sharded here: "replicas only" for this workload).  Timed: the PQR calls only."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_13393_b200 import arnoldi, inputs, pqr
+    from paper_2204_13393_b200 import dist as pdist
+
+    w = WORKLOADS["arnoldi"]
+    g, s, steps = w["grid"], w["s"], w["steps"]
+    n = g ** 3
+    stream = torch.cuda.current_stream(device)
+    R = inputs.device_gaussian(SEED + 2 + 1000 * rank, n, s, device)
+    variants = ["cholqr2", "tsqr"] if args.variant == "both" else [args.variant]
+    acc = {"pqr": 0.0, "op": 0.0}
+    evs = []
+
+    def timer(kind, fn):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r = fn()
+        b.record(stream)
+        evs.append((kind, a, b))
+        return r
+
+    def one_step(prof=False):
+        out = {}
+        for v in variants:
+            res = arnoldi.block_arnoldi(g, g, g, R, steps, variant=v, stream=stream, timer=timer, profile=prof)
+            out[v] = (res["t_list"], res["h"].profile() if prof else None)
+            res["h"].close()
+        return out
+
+    for _ in range(args.warmup):
+        one_step()
+    evs.clear()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        profs = [one_step(prof=True) for _ in range(args.steps)]
+        torch.cuda.synchronize()
+    for kind, a, b in evs:
+        acc[kind] += a.elapsed_time(b)
+    pqr_ms = pdist.max_over_ranks(acc["pqr"] / args.steps, device)
+    op_ms = acc["op"] / args.steps
+    # mandatory bytes of the calls: k = 0 (start), then k = 4, 8, ..., 4*steps
+    mand = sum(mandatory_bytes(n, k, s) for k in range(0, s * steps + 1, s)) * len(variants) * world
+    value = mand / (pqr_ms * 1e-3) / 1e9
+    hbm, peak_kind = peaks()
+    kinds = {}
+    for pr in profs:
+        for v, (tl, p) in pr.items():
+            for kind, d in (p or {}).items():
+                if d["launches"]:
+                    kk = kinds.setdefault(kind, dict(ms=0.0, launches=0))
+                    kk["ms"] += d["ms"]
+                    kk["launches"] += d["launches"]
+    tot = sum(d["ms"] for d in kinds.values()) or 1.0
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": pqr_ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "arnoldi", "baseline_config": 2, "grid": g, "n_local": n, "s": s,
+                           "pqr_calls": steps + 1, "k_range": [0, s * steps], "variants": variants,
+                           "parallelism": f"replicas{world}", "operator_ms_per_step": op_ms,
+                           "l2": "inputs exceed L2 (no flush needed)"},
+                "frac_of_roofline": (mand / world / (hbm * 1e9) * 1e3) / pqr_ms,
+                "kernel_share": {k: d["ms"] / tot for k, d in kinds.items()},
+                "cpu_baseline": None, "e2e": None,
+                "gpu_launches": sum(d["launches"] for d in kinds.values()) // max(1, args.steps),
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -15,7 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 
-def block_arnoldi(nx, ny, nz, R, steps, variant="cholqr2", device="cuda", stream=None, timer=None):
+def block_arnoldi(nx, ny, nz, R, steps, variant="cholqr2", device="cuda", stream=None, timer=None, profile=False):
     """Run Alg. 1.  R: n x s column-major device tensor.  Returns dict(H, k, t_list, handle_stats,
     V_last) and keeps the basis in the handle (returned open as 'h' for further queries).
 
@@ -27,6 +27,8 @@ def block_arnoldi(nx, ny, nz, R, steps, variant="cholqr2", device="cuda", stream
     n = nx * ny * nz
     s = R.shape[1]
     h = pqr.PQR(n, steps * s, s, None, k=0, variant=variant, stream=stream)
+    if profile:
+        h.profile(True)
     run = timer or (lambda kind, fn: fn())
     U = inputs.colmajor_empty(n, s, device)
     Nb = inputs.colmajor_empty(s, s, device)

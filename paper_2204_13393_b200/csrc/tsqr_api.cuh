@@ -41,10 +41,11 @@ struct TsqrState {
 
 int uw_for(int64_t rows) { return (int)((rows + kWyRowsPerUW - 1) / kWyRowsPerUW); }
 int rp_for(int UW) { return kWyRowsPerUW * UW + 10; }  // >= rows, = 10 (mod 16)
-size_t wy_smem(int RP, int wmax, int cap) {
-  return ((size_t)2 * RP * wmax + kWyWarps * 256 + 256 + 256 + 64 + 16 * cap) * sizeof(double) +
-         (size_t)(cap + 1) * sizeof(int2);
+size_t wy_smem(int RP, int wmax, int cap, int nbuf) {
+  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * wmax * wmax + 256 + 256 + 64) * sizeof(double) +
+         (size_t)((cap + 2) & ~1) * sizeof(int2) + 4 * sizeof(uint64_t);
 }
+int nbuf_for(int RP, int wmax, int cap) { return wy_smem(RP, wmax, cap, 3) <= (size_t)kSmemBudget ? 3 : 2; }
 
 template <int UW, int NT>
 cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, size_t smem, cudaStream_t st) {
@@ -76,7 +77,7 @@ WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
   WyLevel L{};
   L.q = lv.q; L.rem2 = lv.rem2; L.odd_last = lv.odd_last; L.nblocks = lv.nblocks;
   L.V = lv.V; L.ldv = lv.ldv; L.T = lv.T; L.tstride = lv.tstride;
-  L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax;
+  L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax; L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap);
   return L;
 }
 
@@ -87,7 +88,7 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   L.X = X; L.ldx = ldx; L.out = out; L.ldo = ldo;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
-  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap);
+  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
   cudaError_t e;
 #define UPC(U, N) wy_up_t<U, N>(L, P, C, s, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, UPC)
@@ -107,7 +108,7 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
   L.cin = cin; L.ldci = ldci; L.Y = Y; L.ldy = ldy;
   WyPanels P{ts->d_pan, np};
   const int NT = ncol > 8 ? 2 : 1;
-  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap);
+  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
   cudaError_t e;
 #define DNC(U, N) wy_down_t<U, N>(L, P, Call, t, ncol, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, DNC)
@@ -224,7 +225,7 @@ int alloc_level(Ctx* h, TsqrLv& lv, int wmax, bool with_io) {
   int rc;
   lv.UW = uw_for(lv.q + 2 * (lv.rem2 > 0) + lv.odd_last);
   lv.RP = rp_for(lv.UW);
-  if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || wy_smem(lv.RP, wmax, ts->cap) > (size_t)kSmemBudget) return PQR_EPLAN;
+  if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || wy_smem(lv.RP, wmax, ts->cap, 2) > (size_t)kSmemBudget) return PQR_EPLAN;
   lv.tstride = (int64_t)16 * ts->cap;
   if (lv.owns_v && (rc = dalloc(&lv.V, (size_t)lv.rows * ts->cap))) return rc;
   if ((rc = dalloc(&lv.T, (size_t)lv.nblocks * lv.tstride))) return rc;
@@ -243,7 +244,7 @@ int tsqr_alloc(Ctx* h) {
   ts->wmax = h->cfg.s_max > 8 ? 16 : 8;
   const int wmax = ts->wmax;
   // node arity: even, node rows within the register/shared-memory budget
-  const int rmax = wmax > 8 ? 512 : 1280;
+  const int rmax = wmax > 8 ? 512 : 1024;
   ts->arity = std::max(2, std::min(8, (rmax / cap) & ~1));
   // leaf block rows: user's choice or ~1024 (512 when s_max > 8)
   int nb = h->cfg.block_rows > 0 ? h->cfg.block_rows : (wmax > 8 ? 512 : 1024);

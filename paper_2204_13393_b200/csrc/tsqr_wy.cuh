@@ -43,6 +43,7 @@ struct WyLevel {
   int cap;
   int RP;                           // smem panel stride (>= max block rows, = 10 mod 16)
   int wmax;                         // widest panel (<= 16) -> smem panel buffer width
+  int nbuf;                         // panel buffers (2 or 3)
 };
 
 struct WyPanels {
@@ -76,7 +77,7 @@ PQR_DEV void wy_load_panel(double* buf, const WyLevel& L, int64_t r0, int R, int
 // Block-wide: Z (w8 x s8, smem, col-major ld 16) = sum over warps of the D fragments
 // acc[mt][nt][2]; red is kWyWarps*256 doubles.  Ends with a __syncthreads.
 template <int NT>
-PQR_DEV void wy_reduce_Z(double (&acc)[2][NT][2], int mtn, double* red, double* Z) {
+PQR_DEV void wy_reduce_Z(double (&acc)[2][NT][2], int mtn, double* red, double* Z, int wm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
 #pragma unroll
@@ -86,13 +87,16 @@ PQR_DEV void wy_reduce_Z(double (&acc)[2][NT][2], int mtn, double* red, double* 
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int i = 8 * mt + g, c = 8 * nt + 2 * q + v;
-        red[warp * 256 + i + 16 * c] = (mt < mtn) ? acc[mt][nt][v] : 0.0;
+        if (i < wm && c < wm) red[warp * wm * wm + i + wm * c] = (mt < mtn) ? acc[mt][nt][v] : 0.0;
       }
   __syncthreads();
   for (int e = threadIdx.x; e < 256; e += kWyThreads) {
+    const int i = e & 15, c = e >> 4;
     double a = 0.0;
+    if (i < wm && c < wm) {
 #pragma unroll
-    for (int w = 0; w < kWyWarps; ++w) a += red[w * 256 + e];
+      for (int w = 0; w < kWyWarps; ++w) a += red[w * wm * wm + i + wm * c];
+    }
     Z[e] = a;
   }
   __syncthreads();
@@ -102,7 +106,7 @@ PQR_DEV void wy_reduce_Z(double (&acc)[2][NT][2], int mtn, double* red, double* 
 //   x <- x - V (Tp Z),  Z = V^T x,  Tp = T^T (stage 1) or T (stage 2);  Tg in smem (ld w)
 template <int UW, int NT>
 PQR_DEV void wy_apply_panel(double (&x)[UW][NT][4], const double* vb, const double* Tg, int w, bool transT,
-                            int RP, double* red, double* Zp) {
+                            int RP, double* red, double* Zp, int wm) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   const int mtn = (w + 7) >> 3;
@@ -141,23 +145,30 @@ PQR_DEV void wy_apply_panel(double (&x)[UW][NT][4], const double* vb, const doub
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int i = 8 * mt + g, c = 8 * nt + 2 * q + v;
-        red[warp * 256 + i + 16 * c] = (mt < mtn) ? acc[0][mt][nt][v] + acc[1][mt][nt][v] : 0.0;
+        if (i < wm && c < wm) red[warp * wm * wm + i + wm * c] = (mt < mtn) ? acc[0][mt][nt][v] + acc[1][mt][nt][v] : 0.0;
       }
   __syncthreads();
-  // ---- Z' = T^T Z (stage 1) or T Z (stage 2), Z = sum over warps of red ----
-  for (int e = tid; e < 256; e += kWyThreads) {
-    const int i = e & 15, c = e >> 4;
-    double a = 0.0;
-    if (i < w) {
-      const int l0 = transT ? 0 : i, l1 = transT ? i : w - 1;
-      for (int l = l0; l <= l1; ++l) {
-        double z = 0.0;
+  // ---- Z = sum over warps of red (fixed order), then Z' = T^T Z (stage 1) or T Z (stage 2) ----
+  const int E = wm * wm;
+  double* Zs = red + kWyWarps * E;  // E doubles after the per-warp partials
+  if (tid < E) {
+    double z = 0.0;
 #pragma unroll
-        for (int ww = 0; ww < kWyWarps; ++ww) z += red[ww * 256 + l + 16 * c];
-        a += (transT ? Tg[l + i * w] : Tg[i + l * w]) * z;
+    for (int ww = 0; ww < kWyWarps; ++ww) z += red[ww * E + tid];
+    Zs[tid] = z;
+  }
+  __syncthreads();
+  if (tid < 256) {
+    const int i = tid & 15, c = tid >> 4;
+    double a = 0.0;
+    if (i < w && c < wm) {
+      if (transT) {
+        for (int l = 0; l <= i; ++l) a += Tg[l + i * w] * Zs[l + wm * c];
+      } else {
+        for (int l = i; l < w; ++l) a += Tg[i + l * w] * Zs[l + wm * c];
       }
     }
-    Zp[e] = a;
+    Zp[tid] = a;
   }
   __syncthreads();
   // ---- x^T -= Z'^T V^T ----
@@ -184,40 +195,65 @@ PQR_DEV void wy_apply_panel(double (&x)[UW][NT][4], const double* vb, const doub
 }
 
 // Apply the first np panels, forward (stage 1, H_0 first, T^T) or reversed (stage 2, T).
-// The panel list and this block's T factors are staged in shared memory (Ts, 16*cap
-// doubles; pans, np entries); panels are double-buffered with cp.async.
+// Panels (and each panel's T, w x w) stream through L.nbuf shared-memory buffers: one
+// thread issues one cp.async.bulk per panel column (R rows, contiguous in HBM: 8 KB at
+// R = 1024, long enough for the bulk-copy engine) plus one for T, completing on the
+// buffer's mbarrier; while panel i is applied, panels i+1 .. i+nbuf-1 are in flight.
+// Rows R..(256*UW)-1 and columns w..w8-1 of every buffer are zeroed once (never copied).
 template <int UW, int NT>
 PQR_DEV void wy_apply_panels(double (&x)[UW][NT][4], const WyLevel& L, const WyPanels& P, int64_t b, int64_t r0,
-                             int R, bool forward, double* vbuf, double* red, double* Zp, double* Ts, int2* pans) {
+                             int R, bool forward, double* vbuf, double* red, double* Zp, int2* pans,
+                             uint64_t* full) {
   const int np = P.np;
   if (np == 0) return;
-  const int RP = L.RP;
-  const int pstride = RP * L.wmax;
+  const int RP = L.RP, nbuf = L.nbuf, wm = L.wmax;
+  const int bstride = RP * wm + 256;  // panel + its T
+  const int Reven = R & ~1;           // rows moved by the bulk copies
   for (int i = threadIdx.x; i < np; i += kWyThreads) pans[i] = P.pan[i];
+  // zero the never-copied parts: rows >= Reven of every column (row R-1 of an odd block is
+  // loaded per element below), all rows of columns >= w are zeroed per panel if w < w8
+  for (int e = threadIdx.x; e < nbuf * wm * (RP - Reven); e += kWyThreads) {
+    const int bb = e / (wm * (RP - Reven)), rem = e % (wm * (RP - Reven));
+    const int j = rem / (RP - Reven), row = Reven + rem % (RP - Reven);
+    vbuf[bb * bstride + j * RP + row] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nbuf; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
   const double* Tb = L.T + b * L.tstride;
   __syncthreads();
-  const int2 last = pans[np - 1];
-  const int tlen = 16 * last.x + last.y * last.y;  // T area used by the panels
-  for (int e = threadIdx.x; e < tlen; e += kWyThreads) Ts[e] = Tb[e];
   auto pidx = [&](int i) { return forward ? i : np - 1 - i; };
-  {
-    const int2 pn = pans[pidx(0)];
-    wy_load_panel<UW>(vbuf, L, r0, R, pn.x, pn.y, RP);
-    cp_async_commit();
-  }
-  for (int i = 0; i < np; ++i) {
-    if (i + 1 < np) {
-      const int2 pn = pans[pidx(i + 1)];
-      wy_load_panel<UW>(vbuf + ((i + 1) & 1) * pstride, L, r0, R, pn.x, pn.y, RP);
+  auto issue = [&](int i) {  // thread 0 only
+    if (i < np) {
+      const int2 pn = pans[pidx(i)];
+      double* buf = vbuf + (i % nbuf) * bstride;
+      uint64_t* bar = &full[i % nbuf];
+      const uint32_t tbytes = (uint32_t)((pn.y * pn.y + 1) & ~1) * 8u;
+      mbar_arrive_expect_tx(bar, (uint32_t)pn.y * Reven * 8u + tbytes);
+      for (int j = 0; j < pn.y; ++j)
+        bulk_g2s(buf + j * RP, L.V + (int64_t)(pn.x + j) * L.ldv + r0, (uint32_t)Reven * 8u, bar);
+      bulk_g2s(buf + RP * wm, Tb + 16 * pn.x, tbytes, bar);
     }
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nbuf - 1; ++i) issue(i);
+  for (int i = 0; i < np; ++i) {
     const int2 pc = pans[pidx(i)];
-    wy_apply_panel<UW, NT>(x, vbuf + (i & 1) * pstride, Ts + 16 * pc.x, pc.y, forward, RP, red, Zp);
-    __syncthreads();  // the buffer is refilled two iterations later
+    double* buf = vbuf + (i % nbuf) * bstride;
+    // per-element pieces: the odd last row, and zero columns w..w8-1 (stale from a wider panel)
+    if (R & 1)
+      for (int j = threadIdx.x; j < pc.y; j += kWyThreads) buf[j * RP + R - 1] = L.V[(int64_t)(pc.x + j) * L.ldv + r0 + R - 1];
+    const int w8 = (pc.y + 7) & ~7;
+    for (int e = threadIdx.x; e < (w8 - pc.y) * Reven; e += kWyThreads) buf[(pc.y + e / Reven) * RP + e % Reven] = 0.0;
+    fence_proxy_async_smem();  // order these generic writes before later bulk copies into the buffer
+    mbar_wait(&full[i % nbuf], (uint32_t)(i / nbuf) & 1u);
+    __syncthreads();          // panel i complete and visible; every warp is done with panel i-1
+    if (threadIdx.x == 0) issue(i + nbuf - 1);  // refill the buffer panel i-1 used
+    wy_apply_panel<UW, NT>(x, buf, buf + RP * wm, pc.y, forward, RP, red, Zp, wm);
   }
-  cp_async_wait<0>();
+  __syncthreads();
 }
 
 // ----------------------------------------------------------------------------
@@ -227,13 +263,13 @@ template <int UW, int NT>
 __global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s) {
   extern __shared__ __align__(16) double sm[];
   const int RP = L.RP;
-  double* vbuf = sm;                                   // 2 x RP x wmax
-  double* red = vbuf + 2 * RP * L.wmax;                // 8 x 256
-  double* Z = red + kWyWarps * 256;                    // 256
+  double* vbuf = sm;                                   // nbuf x (RP x wmax + 256)
+  double* red = vbuf + L.nbuf * (RP * L.wmax + 256);   // (kWyWarps + 1) x wmax^2
+  double* Z = red + (kWyWarps + 1) * L.wmax * L.wmax;  // 256
   double* Zp = Z + 256;                                // 256
   double* bc = Zp + 256;                               // 64 scratch
-  double* Ts = bc + 64;                                // 16 * cap: this block's T factors
-  int2* pans = reinterpret_cast<int2*>(Ts + 16 * L.cap);  // panel list
+  int2* pans = reinterpret_cast<int2*>(bc + 64);       // panel list (cap + 1)
+  uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));  // nbuf mbarriers
   double* Vn = vbuf;                                   // RP x s8: the new reflectors (aliases the
                                                        // panel buffers, free after the panels)
   const int64_t b = blockIdx.x;
@@ -252,7 +288,7 @@ __global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, 
         const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
         x[u][nt][i] = (row < R && c < s) ? L.X[r0 + row + (int64_t)c * L.ldx] : 0.0;
       }
-  wy_apply_panels<UW, NT>(x, L, P, b, r0, R, true, vbuf, red, Zp, Ts, pans);
+  wy_apply_panels<UW, NT>(x, L, P, b, r0, R, true, vbuf, red, Zp, pans, full);
 
   // ---- Householder QR of rows C..R-1 of the s new columns ----
   __syncthreads();
@@ -398,7 +434,7 @@ __global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, 
         }
       }
     }
-    wy_reduce_Z<2>(acc, mtn, red, Z);  // Z = V^T V (16 x 16, ld 16)
+    wy_reduce_Z<2>(acc, mtn, red, Z, L.wmax);  // Z = V^T V (16 x 16, ld 16)
     // T^{-1} = I/2 + striu(V^T V);  T = its inverse (upper triangular), column c by lane c
     double* Tn = L.T + b * L.tstride + 16 * C;
     if (tid < s) {
@@ -425,11 +461,11 @@ __global__ void __launch_bounds__(kWyThreads, 1) k_wy_down(WyLevel L, WyPanels P
   extern __shared__ __align__(16) double sm[];
   const int RP = L.RP;
   double* vbuf = sm;
-  double* red = vbuf + 2 * RP * L.wmax;
-  double* Z = red + kWyWarps * 256;
+  double* red = vbuf + L.nbuf * (RP * L.wmax + 256);
+  double* Z = red + (kWyWarps + 1) * L.wmax * L.wmax;
   double* Zp = Z + 256;
-  double* Ts = Zp + 256 + 64;
-  int2* pans = reinterpret_cast<int2*>(Ts + 16 * L.cap);
+  int2* pans = reinterpret_cast<int2*>(Zp + 256 + 64);
+  uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));
   const int64_t b = blockIdx.x;
   const int64_t r0 = wy_start(L, b);
   const int R = wy_rows(L, b);
@@ -446,7 +482,7 @@ __global__ void __launch_bounds__(kWyThreads, 1) k_wy_down(WyLevel L, WyPanels P
         const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
         y[u][nt][i] = (row < Call && row < R && c < t) ? cb[row + (int64_t)c * L.ldci] : 0.0;
       }
-  wy_apply_panels<UW, NT>(y, L, P, b, r0, R, false, vbuf, red, Zp, Ts, pans);
+  wy_apply_panels<UW, NT>(y, L, P, b, r0, R, false, vbuf, red, Zp, pans, full);
 #pragma unroll
   for (int u = 0; u < UW; ++u)
 #pragma unroll
