@@ -56,7 +56,6 @@ constexpr int kSMaxTop = 16;
 __global__ void __launch_bounds__(256) k_tsqr_top(TsqrTopArgs a) {
   __shared__ double sB[kTopMaxRows * kSMaxTop];
   __shared__ double sV[kTopMaxRows * kSMaxTop];  // reflectors of the top HH
-  __shared__ double sN[kSMaxTop * kSMaxTop];
   __shared__ double sdiag[kSMaxTop];
   __shared__ int spiv[kSMaxTop];
   __shared__ int sT;

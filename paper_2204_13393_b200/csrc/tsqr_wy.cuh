@@ -290,107 +290,16 @@ __global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, 
       }
   wy_apply_panels<UW, NT>(x, L, P, b, r0, R, true, vbuf, red, Zp, pans, full);
 
-  // ---- Householder QR of rows C..R-1 of the s new columns ----
+  // ---- Householder QR of rows C..R-1 of the s new columns (Alg. 6 lines 2-9) ----
+  // The block is moved from the MMA register layout to shared memory (xs, column-major),
+  // where thread t owns rows t, t+512, ...: every thread takes part in each column's
+  // reductions.  Two block barriers per column: red1 carries column c's norm partials
+  // (written right after column c's last update), red2 the dot products of v_c with the
+  // later columns; the buffers alternate, so no third barrier is needed.
+  const int s8 = (s + 7) & ~7;
+  double* xs = vbuf + RP * s8;   // RP x s8 (Vn = vbuf holds the new reflectors)
   __syncthreads();
-  for (int e = tid; e < RP * ((s + 7) & ~7); e += kWyThreads) Vn[e] = 0.0;
-  __syncthreads();
-  for (int c = 0; c < s; ++c) {
-    const int r = C + c;
-    const int ntc = c >> 3, gc = c & 7;
-    // lambda^2 over rows >= r of column c, and u0 = x[r][c]
-    double part = 0.0;
-    if (g == gc) {
-#pragma unroll
-      for (int u = 0; u < UW; ++u)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          if (nt == ntc)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int row = 16 * (warp * UW + u) + 4 * q + i;
-              if (row >= r && row < R) part += x[u][nt][i] * x[u][nt][i];
-              if (row == r) bc[0] = x[u][nt][i];
-            }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    double lam2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWyWarps; ++w) lam2 += red[w];
-    const double lam = sqrt(lam2);
-    const double u0 = bc[0];
-    const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
-    const double diag = sigma * lam;
-    const double nv2 = 2.0 * lam * (lam + fabs(u0));
-    const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lam == 0 (R4)
-    // v on this lane's rows (valid in lanes g == gc); column c becomes [x(0:r); diag; 0]
-    double vv[UW][4];
-#pragma unroll
-    for (int u = 0; u < UW; ++u)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = 16 * (warp * UW + u) + 4 * q + i;
-        double xv = 0.0;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          if (nt == ntc) xv = x[u][nt][i];
-        const double v = (row > r && row < R) ? xv * inv : (row == r ? (xv - diag) * inv : 0.0);
-        vv[u][i] = v;
-        if (g == gc) {
-          if (row < R) Vn[c * RP + row] = v;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            if (nt == ntc && row >= r) x[u][nt][i] = (row == r) ? diag : 0.0;
-        }
-      }
-    // apply H = I - 2 v v^T to columns c+1..s-1: lanes of column c' fetch v from lane (gc, q)
-    if (c + 1 < s) {
-#pragma unroll
-      for (int u = 0; u < UW; ++u)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) vv[u][i] = __shfl_sync(0xffffffffu, vv[u][i], gc * 4 + q);
-      double dp[NT];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        double a = 0.0;
-        if (8 * nt + g > c) {
-#pragma unroll
-          for (int u = 0; u < UW; ++u)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a += vv[u][i] * x[u][nt][i];
-        }
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        dp[nt] = a;
-      }
-      __syncthreads();  // red[] reads of the norm step are done
-      if (q == 0) {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) red[warp * 16 + 8 * nt + g] = dp[nt];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int cc = 8 * nt + g;
-        if (cc > c && cc < s) {
-          double d = 0.0;
-#pragma unroll
-          for (int w = 0; w < kWyWarps; ++w) d += red[w * 16 + cc];
-          const double f = 2.0 * d;
-#pragma unroll
-          for (int u = 0; u < UW; ++u)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) x[u][nt][i] -= f * vv[u][i];
-        }
-      }
-    }
-    __syncthreads();  // red / bc reuse
-  }
-
-  // ---- outputs: [P_b; N_b] = rows 0..C+s-1, the new reflectors, the new panel's T ----
-  double* outb = L.out + b * L.cap;
+  for (int e = tid; e < RP * s8; e += kWyThreads) Vn[e] = 0.0;
 #pragma unroll
   for (int u = 0; u < UW; ++u)
 #pragma unroll
@@ -398,8 +307,86 @@ __global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, 
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
-        if (row < C + s && row < R && c < s) outb[row + (int64_t)c * L.ldo] = x[u][nt][i];
+        if (c < s8) xs[c * RP + row] = x[u][nt][i];
       }
+  constexpr int RPT = (kWyRowsPerUW * UW + kWyThreads - 1) / kWyThreads;  // rows per thread
+  double* red1 = red;          // kWyWarps
+  double* red2 = red + 64;     // kWyWarps x 16
+  auto norm_partial = [&](int c) {
+    const int r = C + c;
+    double part = 0.0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int row = tid + j * kWyThreads;
+      if (row >= r && row < R) part += xs[c * RP + row] * xs[c * RP + row];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) red1[warp] = part;
+  };
+  __syncthreads();
+  if (s > 0) norm_partial(0);
+  for (int c = 0; c < s; ++c) {
+    const int r = C + c;
+    __syncthreads();  // S1: norm partials of column c in red1; column c final above row r
+    double lam2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWyWarps; ++w) lam2 += red1[w];
+    const double lam = sqrt(lam2);
+    const double u0 = r < R ? xs[c * RP + r] : 0.0;
+    const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
+    const double diag = sigma * lam;
+    const double nv2 = 2.0 * lam * (lam + fabs(u0));
+    const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lam == 0 (R4)
+    double v[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int row = tid + j * kWyThreads;
+      const double xv = row < R ? xs[c * RP + row] : 0.0;
+      v[j] = (row > r && row < R) ? xv * inv : (row == r ? (xv - diag) * inv : 0.0);
+    }
+    // dot products v . x[:, c'] for c' > c (reduced over the warp, then over warps)
+    for (int cc = c + 1; cc < s; ++cc) {
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int row = tid + j * kWyThreads;
+        if (row < R) a += v[j] * xs[cc * RP + row];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) red2[warp * 16 + cc] = a;
+    }
+    __syncthreads();  // S2: dots in red2; every thread has read u0 and red1
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int row = tid + j * kWyThreads;
+      if (row < R) {
+        Vn[c * RP + row] = v[j];
+        if (row >= r) xs[c * RP + row] = (row == r) ? diag : 0.0;
+      }
+    }
+    for (int cc = c + 1; cc < s; ++cc) {
+      double d = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWyWarps; ++w) d += red2[w * 16 + cc];
+      const double f = 2.0 * d;
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int row = tid + j * kWyThreads;
+        if (row < R) xs[cc * RP + row] -= f * v[j];
+      }
+    }
+    if (c + 1 < s) norm_partial(c + 1);
+  }
+  __syncthreads();
+
+  // ---- outputs: [P_b; N_b] = rows 0..C+s-1, the new reflectors, the new panel's T ----
+  double* outb = L.out + b * L.cap;
+  for (int e = tid; e < s * (C + s); e += kWyThreads) {
+    const int c = e / (C + s), row = e - c * (C + s);
+    if (row < R) outb[row + (int64_t)c * L.ldo] = xs[c * RP + row];
+  }
   for (int e = tid; e < s * R; e += kWyThreads) {
     const int c = e / R, row = e - c * R;
     L.V[r0 + row + (int64_t)(C + c) * L.ldv] = Vn[c * RP + row];
