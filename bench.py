@@ -317,6 +317,7 @@ def main():
     per_launch_bytes = {
         "gram": 8.0 * n * (k + s),             # read Q, X (or Q, U1)
         "update": 8.0 * n * (k + s) + 8.0 * n * s,  # read Q, X; write U
+        "update_gram": 8.0 * n * (k + s) + 8.0 * n * s,  # read Q, X; write U1 (W2 on chip)
         "tsqr_local": 8.0 * n * (k + s) + 8.0 * n * s,  # read Y (reflectors) and X, write new reflectors
         "tsqr_apply": 8.0 * n * (k + s) + 8.0 * n * s,  # read Y, write U
     }

@@ -130,7 +130,8 @@ int pqr_get_stats(pqr_handle h, pqr_stats* st);
 #define PQR_K_TSQR_TREE   5   /* a7 TSQR reduction tree (up + down sweeps)  */
 #define PQR_K_TSQR_APPLY  6   /* a8 TSQR stage-2 LOR apply                  */
 #define PQR_K_OTHER       7   /* copies / staging                           */
-#define PQR_NUM_KINDS     8
+#define PQR_K_UPDATE_GRAM 8   /* a4+a1 fused second CholQR pass              */
+#define PQR_NUM_KINDS     9
 typedef struct {
   double ms[PQR_NUM_KINDS];       /* summed device milliseconds per kind */
   int64_t launches[PQR_NUM_KINDS];

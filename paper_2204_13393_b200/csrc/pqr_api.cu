@@ -343,8 +343,60 @@ int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches) {
   return PQR_OK;
 }
 
+// Fused second CholQR pass: U1 = [Q X] M1 (into U1) and W2 = [Q U1]^T U1 (into W).
+// Returns PQR_EPLAN when the fused kernel cannot be used (caller falls back).
+template <int MTH, int NT>
+cudaError_t launch_update_gram_t(int grid, size_t smem, const UpdGramArgs& a, cudaStream_t st) {
+  auto f = k_update_gram_cpa<MTH, NT>;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  f<<<grid, kCpaThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+int run_update_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double* X, int64_t ldx,
+                    const double* M, int ldm, const int* t_dev, double* U1, int64_t ldu, double* W, int ldw,
+                    double* partials, unsigned int* ticket, int sms, cudaStream_t st, int64_t* launches) {
+  static const bool disabled = getenv("PQR_NO_FUSE") != nullptr;
+  const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (ldx & 1) == 0 && aligned16(X) &&
+                   (ldu & 1) == 0 && aligned16(U1);
+  const int m = k + s, MT = (m + 7) / 8, MTH = (MT + 1) / 2, NT = s > 8 ? 2 : 1;
+  const int KS = (m + 3) / 4, mpad = KS * 4;
+  const size_t stage_bytes = (size_t)MT * 8 * kFuseRBP * sizeof(double);
+  const size_t extra = ((size_t)NT * mpad * 8 + 8 * NT * kFuseRBP + kCpaWarps * NT * 128) * sizeof(double);
+  const size_t red_bytes = (size_t)kCpaWarps * MTH * NT * 64 * sizeof(double);
+  static const int env_ctas = getenv("PQR_FUSE_CTAS") ? atoi(getenv("PQR_FUSE_CTAS")) : 2;
+  const int ctas = env_ctas == 1 ? 1 : 2;
+  const size_t budget = ctas == 2 ? kSmemBudget / 2 - 2048 : kSmemBudget;
+  int NS = budget > extra ? (int)std::min<size_t>(8, (budget - extra) / (stage_bytes + 16)) : 0;
+  while (NS >= 2 && (size_t)NS * stage_bytes < red_bytes) ++NS;
+  const size_t smem = std::max((size_t)NS * stage_bytes, red_bytes) + extra + 2 * NS * sizeof(uint64_t);
+  if (disabled || !vec || MTH > 10 || NS < 2 || smem > budget) return PQR_EPLAN;
+  UpdGramArgs a{};
+  a.Q = Q; a.ldq = ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.NS = NS;
+  a.M = M; a.ldm = ldm; a.t_dev = t_dev; a.U1 = U1; a.ldu = ldu;
+  a.partials = partials; a.W = W; a.ldw = ldw; a.ticket = ticket;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * ctas, (n + kFuseRB - 1) / kFuseRB));
+  cudaError_t e;
+#define PQR_FUSE_CASE(H)                                                                    \
+  case H * 10 + 1: e = launch_update_gram_t<H, 1>(grid, smem, a, st); break;               \
+  case H * 10 + 2: e = launch_update_gram_t<H, 2>(grid, smem, a, st); break;
+  switch (MTH * 10 + NT) {
+    PQR_FUSE_CASE(1) PQR_FUSE_CASE(2) PQR_FUSE_CASE(3) PQR_FUSE_CASE(4) PQR_FUSE_CASE(5)
+    PQR_FUSE_CASE(6) PQR_FUSE_CASE(7) PQR_FUSE_CASE(8) PQR_FUSE_CASE(9) PQR_FUSE_CASE(10)
+    default: return PQR_EPLAN;
+  }
+#undef PQR_FUSE_CASE
+  if (launches) ++*launches;
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[pqr] update+gram launch: %s\n", cudaGetErrorString(e));
+    return PQR_ECUDA;
+  }
+  return PQR_OK;
+}
+
 // Gram of this rank, then (nranks > 1) allgather so every rank sums all ranks'
 // partial Grams in rank order inside k_factor (bitwise identical replicas).
+int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts);
 int gram_and_exchange(Ctx* h, int k, int s, const double* Q, const double* X, int64_t ldx, const double** Wsum,
                       int* nparts) {
   const int m = k + s;
@@ -353,6 +405,11 @@ int gram_and_exchange(Ctx* h, int k, int s, const double* Q, const double* X, in
     TRY(run_gram(h->cfg.n_local, k, s, Q, h->ld, X, ldx, h->Wloc, m, h->partials, h->ticket, h->sms, h->stream,
                  &h->st.kernel_launches));
   }
+  return exchange(h, m, s, Wsum, nparts);
+}
+
+// (nranks > 1) allgather this rank's Gram so every rank sums all ranks' in rank order
+int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts) {
   if (h->cfg.nranks > 1) {
     PROF(h, PQR_K_NCCL);
     NCCL_TRY(ncclAllGather(h->Wloc, h->Wall, (size_t)m * s, ncclDouble, h->comm, h->stream));
@@ -395,14 +452,30 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
     PROF(h, PQR_K_FACTOR);
     TRY(run_factor(f, h->stream, &h->st.kernel_launches));
   }
-  {
+  bool fused = false;
+  if (!single) {
+    // second pass fused with the first update: U1 = [Q X] M1 and W2 = [Q U1]^T U1 in one read
+    int rc;
+    {
+      PROF(h, PQR_K_UPDATE_GRAM);
+      rc = run_update_gram(n, k, s, h->basis, h->ld, X, ldx, h->M1, m, d_t1, Ud, ldud, h->Wloc, m, h->partials,
+                           h->ticket, h->sms, h->stream, &h->st.kernel_launches);
+    }
+    if (rc == PQR_OK) {
+      fused = true;
+      TRY(exchange(h, m, s, &Wsum, &nparts));
+    } else if (rc != PQR_EPLAN) {
+      return rc;
+    }
+  }
+  if (!fused) {
     PROF(h, PQR_K_UPDATE);
     TRY(run_update(n, k, h->basis, h->ld, s, X, ldx, h->M1, m, s, d_t1, Ud, ldud, single ? Uappend : nullptr,
                    h->ld, h->sms, h->stream, &h->st.kernel_launches));
   }
   if (!single) {
     // pass 2 on [Q U1]: W2 -> P2, N2, M2 (+ recombination) -> U = [Q U1] M2 (in place)
-    TRY(gram_and_exchange(h, k, s, h->basis, Ud, ldud, &Wsum, &nparts));
+    if (!fused) TRY(gram_and_exchange(h, k, s, h->basis, Ud, ldud, &Wsum, &nparts));
     FactorArgs f2{};
     f2.W = Wsum; f2.w_stride = (int64_t)m * s; f2.nparts = nparts; f2.ldw = m; f2.k = k; f2.s = s; f2.s_dev = d_t1;
     f2.tol2 = 0.0; f2.eta = 0.0;

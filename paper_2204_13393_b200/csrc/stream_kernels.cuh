@@ -221,6 +221,241 @@ __global__ void __launch_bounds__(kCpaThreads, 2) k_gram_cpa(GramCpaArgs a) {
 }
 
 // ----------------------------------------------------------------------------
+// a4 + a1 fused (second CholQR pass): U1 = [Q X] M1 and W2 = [Q U1]^T U1 in one pass
+// ----------------------------------------------------------------------------
+// Stage = 32 rows x all m columns of [Q X] (as k_gram_cpa).  Per stage:
+//   (U) U1^T = M1^T [Q X]^T for the 32 rows: warp w takes 16-row unit (w & 1) and a
+//       quarter (w >> 1) of the k-steps; the 4 partials per unit are summed in fixed
+//       order into a shared-memory U1 tile, which is also written to HBM (pass 3 reads it);
+//   (G) W2 += [Q U1]^T U1 over the same rows, Q from the stage, U1 from the tile.
+// Q and X are read once for both — the second pass of BCGS-PIP+ (PAPER.md:L521-525,
+// Alg. 8 lines 3-4) costs one read of [Q X] instead of two.
+struct UpdGramArgs {
+  const double* Q; int64_t ldq;
+  const double* X; int64_t ldx;
+  int64_t n; int k; int s; int NS;
+  const double* M; int ldm;       // (k+s) x s: U1 = [Q X] M
+  const int* t_dev;               // valid U1 columns (t1); columns >= t1 are written as zero
+  double* U1; int64_t ldu;        // n x s output
+  double* partials;
+  double* W; int ldw;
+  unsigned int* ticket;
+};
+
+constexpr int kFuseRB = 32;
+constexpr int kFuseRBP = 40;
+
+template <int MTH, int NT>
+__global__ void __launch_bounds__(kCpaThreads, 2) k_update_gram_cpa(UpdGramArgs a) {
+  constexpr int SUBS = kFuseRB / 8, GROUPS = kCpaWarps / SUBS;
+  extern __shared__ __align__(16) double sm[];
+  const int k = a.k, s = a.s, m = k + s, MT = (m + 7) >> 3, mp = MT * 8;
+  const int KS = (m + 3) >> 2, mpad = KS * 4, KQ = (KS + 3) / 4;
+  const int NS = a.NS;
+  const int stage_dbl = mp * kFuseRBP;
+  double* sMm = sm + (size_t)NS * stage_dbl;          // [NT][mpad][8]
+  double* u1t = sMm + (size_t)NT * mpad * 8;          // U1 tile: [8*NT cols][kFuseRBP]
+  double* redU = u1t + 8 * NT * kFuseRBP;             // [8 warps][NT][32 lanes][4]
+  uint64_t* full = reinterpret_cast<uint64_t*>(redU + kCpaWarps * NT * 128);
+  uint64_t* empty = full + NS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, q = lane & 3;
+  const int sub = warp % SUBS, half = warp / SUBS;
+  const int t1 = a.t_dev ? *a.t_dev : s;
+
+  for (int e = tid; e < NS * (mp - m) * kFuseRBP; e += kCpaThreads) {
+    const int st = e / ((mp - m) * kFuseRBP), rem = e % ((mp - m) * kFuseRBP);
+    sm[(size_t)st * stage_dbl + m * kFuseRBP + rem] = 0.0;
+  }
+  for (int e = tid; e < NT * mpad * 8; e += kCpaThreads) {
+    const int nt = e / (mpad * 8), rem = e % (mpad * 8);
+    const int j = rem >> 3, c = 8 * nt + (rem & 7);
+    sMm[e] = (j < m && c < s) ? a.M[j + (int64_t)c * a.ldm] : 0.0;
+  }
+  for (int e = tid; e < 8 * NT * kFuseRBP; e += kCpaThreads) u1t[e] = 0.0;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], kCpaThreads);
+      mbar_init(&empty[i], kCpaWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t nrb = (a.n + kFuseRB - 1) / kFuseRB;
+  const int cnt = blockIdx.x < nrb ? (int)((nrb - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  constexpr int RP = kFuseRB / 2;
+  constexpr int TMAX = (kMMax * RP + kCpaThreads - 1) / kCpaThreads;
+  const double* tsrc[TMAX];
+  int tdst[TMAX];
+  int ntask = 0;
+#pragma unroll
+  for (int t = 0; t < TMAX; ++t) {
+    const int e = tid + t * kCpaThreads;
+    const int j = e / RP, p = e % RP;
+    const bool ok = j < m;
+    tsrc[t] = ok ? col_ptr(a.Q, a.ldq, a.X, a.ldx, k, m, j) + 2 * p : a.X;
+    tdst[t] = ok ? j * kFuseRBP + 2 * p : 0;
+    ntask += ok ? 1 : 0;
+  }
+  int64_t r0_p = (int64_t)blockIdx.x * kFuseRB;
+  const int64_t r0_step = (int64_t)gridDim.x * kFuseRB;
+  auto issue = [&](int it, int st) {
+    if (it < cnt) {
+      double* buf = sm + (size_t)st * stage_dbl;
+      if (r0_p + kFuseRB <= a.n) {
+#pragma unroll
+        for (int t = 0; t < TMAX; ++t)
+          if (t < ntask) cp_async16(buf + tdst[t], tsrc[t] + r0_p, 16);
+      } else {
+#pragma unroll
+        for (int t = 0; t < TMAX; ++t)
+          if (t < ntask) {
+            const int64_t row = r0_p + ((tid + t * kCpaThreads) % RP) * 2;
+            const int bytes = row + 1 < a.n ? 16 : (row < a.n ? 8 : 0);
+            cp_async16(buf + tdst[t], bytes ? (const void*)(tsrc[t] + r0_p) : (const void*)a.X, bytes);
+          }
+      }
+      cp_async_mbar_arrive(&full[st]);
+      r0_p += r0_step;
+    }
+  };
+
+  double acc[MTH][NT][2];
+#pragma unroll
+  for (int i = 0; i < MTH; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[i][nt][0] = acc[i][nt][1] = 0.0;
+  for (int it = 0; it < NS - 1; ++it) issue(it, it);
+  const int ro = sub * 8 + 2 * q;
+  // Gram tiles of [Q U1]: lanes whose column is < k read the stage, the others the U1 tile
+  int aoff[MTH];
+  bool ain_u[MTH];
+#pragma unroll
+  for (int i = 0; i < MTH; ++i) {
+    const int mt = half * MTH + i;
+    const int j = mt < MT ? 8 * mt + gq : 0;
+    ain_u[i] = j >= k;
+    aoff[i] = (j >= k ? j - k : j) * kFuseRBP + ro;
+  }
+  int boff[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) boff[nt] = (8 * nt + gq) * kFuseRBP + ro;
+  const int uu = warp & 1, kq = warp >> 1;       // update: unit, k-step quarter
+  const int kk0 = kq * KQ, kk1 = min(KS, kk0 + KQ);
+  int st = 0, ph = 0, stp = NS - 1;
+  int64_t r0 = (int64_t)blockIdx.x * kFuseRB;
+  for (int it = 0; it < cnt; ++it) {
+    if (it >= 1) mbar_wait(&empty[stp], (uint32_t)(((it - 1) / NS) & 1));
+    issue(it + NS - 1, stp);
+    stp = stp + 1 == NS ? 0 : stp + 1;
+    mbar_wait(&full[st], (uint32_t)ph);
+    const double* buf = sm + (size_t)st * stage_dbl;
+    // ---- (U) partial U1^T over this warp's k-steps ----
+    double d[NT][2][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) d[nt][0][0] = d[nt][0][1] = d[nt][1][0] = d[nt][1][1] = 0.0;
+    for (int kk = kk0; kk < kk1; ++kk) {
+      const double2 av = lds2(buf + (4 * kk + q) * kFuseRBP + 16 * uu + 2 * gq);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double mv = sMm[(nt * mpad + 4 * kk + q) * 8 + gq];
+        dmma884(d[nt][0][0], d[nt][0][1], mv, av.x);
+        dmma884(d[nt][1][0], d[nt][1][1], mv, av.y);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double* rp = redU + ((warp * NT + nt) * 32 + lane) * 4;
+      rp[0] = d[nt][0][0]; rp[1] = d[nt][0][1]; rp[2] = d[nt][1][0]; rp[3] = d[nt][1][1];
+    }
+    __syncthreads();
+    // combine the 4 k-quarters of each unit (fixed order) into the U1 tile and HBM
+    for (int e = tid; e < 2 * NT * 128; e += kCpaThreads) {
+      const int u = e / (NT * 128), rest = e % (NT * 128);
+      const int nt = rest / 128, l = (rest % 128) >> 2, v = rest & 3;
+      double val = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) val += redU[(((qq * 2 + u) * NT + nt) * 32 + l) * 4 + v];
+      // v: 0 = even MMA c0 (row 4q), 1 = even c1 (row 4q+2), 2 = odd c0 (4q+1), 3 = odd c1 (4q+3)
+      const int lq = l & 3, lg = l >> 2;
+      const int row = 16 * u + 4 * lq + ((v & 1) ? 2 : 0) + (v >> 1);
+      const int col = 8 * nt + lg;
+      const double w = col < t1 ? val : 0.0;
+      u1t[col * kFuseRBP + row] = w;
+      const int64_t grow = r0 + row;
+      if (col < s && grow < a.n) a.U1[grow + (int64_t)col * a.ldu] = w;
+    }
+    __syncthreads();
+    // ---- (G) W2 += [Q U1]^T U1 over the stage's rows ----
+    double2 bv[NT], avv[MTH];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bv[nt] = lds2(u1t + boff[nt]);
+#pragma unroll
+    for (int i = 0; i < MTH; ++i) avv[i] = lds2((ain_u[i] ? u1t : buf) + aoff[i]);
+#pragma unroll
+    for (int i = 0; i < MTH; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma884(acc[i][nt][0], acc[i][nt][1], avv[i].x, bv[nt].x);
+#pragma unroll
+    for (int i = 0; i < MTH; ++i)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma884(acc[i][nt][0], acc[i][nt][1], avv[i].y, bv[nt].y);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (++st == NS) { st = 0; ph ^= 1; }
+    r0 += r0_step;
+  }
+  __syncthreads();
+  // ---- CTA reduction over the SUBS sub-slab warps of each tile group (fixed order) ----
+  const int per_warp = MTH * NT * 64;
+  double* red = sm;
+#pragma unroll
+  for (int i = 0; i < MTH; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      red[warp * per_warp + ((i * NT + nt) * 32 + lane) * 2 + 0] = acc[i][nt][0];
+      red[warp * per_warp + ((i * NT + nt) * 32 + lane) * 2 + 1] = acc[i][nt][1];
+    }
+  __syncthreads();
+  double* part = a.partials + (size_t)blockIdx.x * m * s;
+  for (int e = tid; e < GROUPS * per_warp; e += kCpaThreads) {
+    const int hf = e / per_warp, r = e % per_warp;
+    const int v = r & 1, l = (r >> 1) & 31, rest = r >> 6;
+    const int nt = rest % NT, i = rest / NT;
+    const int mt = hf * MTH + i;
+    const int jj = 8 * mt + (l >> 2), c = 8 * nt + 2 * (l & 3) + v;
+    if (mt < MT && jj < m && c < s) {
+      double sum = 0.0;
+      for (int sb = 0; sb < SUBS; ++sb) sum += red[(hf * SUBS + sb) * per_warp + r];
+      part[jj + (int64_t)c * m] = sum;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned int s_last;
+  if (tid == 0) s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ms = m * s;
+  const int nb = gridDim.x;
+  for (int e = tid; e < ms; e += kCpaThreads) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = 0;
+    for (; b + 4 <= nb; b += 4) {
+      s0 += __ldcg(a.partials + (size_t)(b + 0) * ms + e);
+      s1 += __ldcg(a.partials + (size_t)(b + 1) * ms + e);
+      s2 += __ldcg(a.partials + (size_t)(b + 2) * ms + e);
+      s3 += __ldcg(a.partials + (size_t)(b + 3) * ms + e);
+    }
+    for (; b < nb; ++b) s0 += __ldcg(a.partials + (size_t)b * ms + e);
+    const int jj = e % m, c = e / m;
+    a.W[jj + (int64_t)c * a.ldw] = (s0 + s1) + (s2 + s3);
+  }
+  if (tid == 0) *a.ticket = 0u;
+}
+
+// ----------------------------------------------------------------------------
 // a4: U = [Q X] M
 // ----------------------------------------------------------------------------
 constexpr int kUpdRB = 128;   // rows per row block (8 warps x 16)

@@ -47,10 +47,10 @@ class pqr_stats(ctypes.Structure):
 
 
 class pqr_profile(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 8), ("launches", ctypes.c_int64 * 8)]
+    _fields_ = [("ms", ctypes.c_double * 9), ("launches", ctypes.c_int64 * 9)]
 
 
-PROFILE_KINDS = ["gram", "factor", "update", "nccl", "tsqr_local", "tsqr_tree", "tsqr_apply", "other"]
+PROFILE_KINDS = ["gram", "factor", "update", "nccl", "tsqr_local", "tsqr_tree", "tsqr_apply", "other", "update_gram"]
 
 EXPORTS = ["pqr_create", "pqr_project_normalize", "pqr_basis_apply", "pqr_destroy", "pqr_strerror",
            "pqr_get_stats", "pqr_profile_enable", "pqr_get_profile", "pqr_nccl_unique_id",
