@@ -67,6 +67,7 @@ class ClockSampler:
 
     def __init__(self, index):
         self.samples = []
+        self.power = []
         self.reasons = set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -86,6 +87,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.hd, self.nv.NVML_CLOCK_SM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.hd) / 1000.0)
                 fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                     getattr(self.nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
                 r = fn(self.hd)
@@ -110,8 +112,11 @@ class ClockSampler:
     def summary(self):
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_min_mhz": min(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power:
+            out["power_w"] = round(statistics.median(self.power), 1)
+        return out
 
 
 # --------------------------------------------------------------------------

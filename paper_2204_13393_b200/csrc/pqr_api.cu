@@ -365,7 +365,7 @@ int run_update_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const
   const size_t extra = ((size_t)NT * mpad * 8 + 8 * NT * kFuseRBP + kCpaWarps * NT * 128) * sizeof(double);
   const size_t red_bytes = (size_t)kCpaWarps * MTH * NT * 64 * sizeof(double);
   static const int env_ctas = getenv("PQR_FUSE_CTAS") ? atoi(getenv("PQR_FUSE_CTAS")) : 2;
-  const int ctas = env_ctas == 1 ? 1 : 2;
+  const int ctas = (env_ctas == 1 || NT > 1) ? 1 : 2;
   const size_t budget = ctas == 2 ? kSmemBudget / 2 - 2048 : kSmemBudget;
   int NS = budget > extra ? (int)std::min<size_t>(8, (budget - extra) / (stage_bytes + 16)) : 0;
   while (NS >= 2 && (size_t)NS * stage_bytes < red_bytes) ++NS;

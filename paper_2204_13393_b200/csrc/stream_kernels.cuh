@@ -246,7 +246,7 @@ constexpr int kFuseRB = 32;
 constexpr int kFuseRBP = 40;
 
 template <int MTH, int NT>
-__global__ void __launch_bounds__(kCpaThreads, 2) k_update_gram_cpa(UpdGramArgs a) {
+__global__ void __launch_bounds__(kCpaThreads, NT == 1 ? 2 : 1) k_update_gram_cpa(UpdGramArgs a) {
   constexpr int SUBS = kFuseRB / 8, GROUPS = kCpaWarps / SUBS;
   extern __shared__ __align__(16) double sm[];
   const int k = a.k, s = a.s, m = k + s, MT = (m + 7) >> 3, mp = MT * 8;
@@ -342,6 +342,12 @@ __global__ void __launch_bounds__(kCpaThreads, 2) k_update_gram_cpa(UpdGramArgs 
   for (int nt = 0; nt < NT; ++nt) boff[nt] = (8 * nt + gq) * kFuseRBP + ro;
   const int uu = warp & 1, kq = warp >> 1;       // update: unit, k-step quarter
   const int kk0 = kq * KQ, kk1 = min(KS, kk0 + KQ);
+  // M1^T fragments of this warp's k-steps, held for the whole kernel (KQ <= MTH)
+  double mreg[MTH][NT];
+#pragma unroll
+  for (int i = 0; i < MTH; ++i)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) mreg[i][nt] = kk0 + i < kk1 ? sMm[(nt * mpad + 4 * (kk0 + i) + q) * 8 + gq] : 0.0;
   int st = 0, ph = 0, stp = NS - 1;
   int64_t r0 = (int64_t)blockIdx.x * kFuseRB;
   for (int it = 0; it < cnt; ++it) {
@@ -354,13 +360,15 @@ __global__ void __launch_bounds__(kCpaThreads, 2) k_update_gram_cpa(UpdGramArgs 
     double d[NT][2][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) d[nt][0][0] = d[nt][0][1] = d[nt][1][0] = d[nt][1][1] = 0.0;
-    for (int kk = kk0; kk < kk1; ++kk) {
-      const double2 av = lds2(buf + (4 * kk + q) * kFuseRBP + 16 * uu + 2 * gq);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double mv = sMm[(nt * mpad + 4 * kk + q) * 8 + gq];
-        dmma884(d[nt][0][0], d[nt][0][1], mv, av.x);
-        dmma884(d[nt][1][0], d[nt][1][1], mv, av.y);
+    for (int i = 0; i < MTH; ++i) {
+      if (kk0 + i < kk1) {
+        const double2 av = lds2(buf + (4 * (kk0 + i) + q) * kFuseRBP + 16 * uu + 2 * gq);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma884(d[nt][0][0], d[nt][0][1], mreg[i][nt], av.x);
+          dmma884(d[nt][1][0], d[nt][1][1], mreg[i][nt], av.y);
+        }
       }
     }
 #pragma unroll
