@@ -40,25 +40,27 @@ struct TsqrState {
 };
 
 int uw_for(int64_t rows) { return (int)((rows + kWyRowsPerUW - 1) / kWyRowsPerUW); }
-int rp_for(int UW) { return kWyRowsPerUW * UW + 10; }  // >= rows, = 10 (mod 16)
-size_t wy_smem(int RP, int wmax, int cap, int nbuf) {
-  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * wmax * wmax + 256 + 256 + 64) * sizeof(double) +
-         (size_t)((cap + 2) & ~1) * sizeof(int2) + 4 * sizeof(uint64_t);
+int rp_for(int UW) { return kWyRowsPerUW * UW + 10; }  // >= rows + 1, = 10 (mod 16)
+size_t wy_smem(int RP, int wmax, int cap, int nbuf) { return wy_smem_bytes(RP, wmax, cap, nbuf); }
+int nbuf_for(int RP, int wmax, int cap) {
+  for (int nb = 4; nb > 2; --nb)
+    if (wy_smem(RP, wmax, cap, nb) <= (size_t)kSmemBudget) return nb;
+  return 2;
 }
-int nbuf_for(int RP, int wmax, int cap) { return wy_smem(RP, wmax, cap, 3) <= (size_t)kSmemBudget ? 3 : 2; }
 
 template <int UW, int NT>
-cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, size_t smem, cudaStream_t st) {
+cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int grid, size_t smem, cudaStream_t st) {
   auto f = k_wy_up<UW, NT>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  f<<<L.nblocks, kWyThreads, smem, st>>>(L, P, C, s);
+  f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s);
   return cudaGetLastError();
 }
 template <int UW, int NT>
-cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, size_t smem, cudaStream_t st) {
+cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
+                      cudaStream_t st) {
   auto f = k_wy_down<UW, NT>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  f<<<L.nblocks, kWyThreads, smem, st>>>(L, P, Call, t, ncol);
+  f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
   return cudaGetLastError();
 }
 
@@ -66,18 +68,37 @@ cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int 
   switch ((UW_) * 10 + (NT_)) {                                                              \
     case 11: e = CALL(1, 1); break; case 12: e = CALL(1, 2); break;                         \
     case 21: e = CALL(2, 1); break; case 22: e = CALL(2, 2); break;                         \
-    case 31: e = CALL(3, 1); break; case 32: e = CALL(3, 2); break;                         \
-    case 41: e = CALL(4, 1); break; case 42: e = CALL(4, 2); break;                         \
-    case 51: e = CALL(5, 1); break; case 52: e = CALL(5, 2); break;                         \
+    case 31: e = CALL(3, 1); break;                                                          \
+    case 41: e = CALL(4, 1); break;                                                          \
+    case 51: e = CALL(5, 1); break;                                                          \
     case 61: e = CALL(6, 1); break;                                                          \
     default: return PQR_EPLAN;                                                               \
   }
+
+// PQR_WY_TRACE=1: per-phase cycle counters of CTA 0 (warps 0 and 15) printed to stderr
+// after every level kernel (tuning aid; serialises the stream).
+unsigned long long* wy_trace_buf() {
+  static unsigned long long* buf = nullptr;
+  static const bool on = getenv("PQR_WY_TRACE") != nullptr;
+  if (on && !buf) cudaMalloc(&buf, 64 * sizeof(unsigned long long));
+  return on ? buf : nullptr;
+}
+void wy_trace_dump(const char* kind, const WyLevel& L, cudaStream_t st) {
+  if (!L.trace) return;
+  unsigned long long h[32];
+  cudaStreamSynchronize(st);
+  cudaMemcpy(h, L.trace, sizeof(h), cudaMemcpyDeviceToHost);
+  fprintf(stderr, "{\"wy_trace\": \"%s\", \"nblocks\": %d, \"rows\": %lld, \"w0\": [", kind, L.nblocks, (long long)L.q);
+  for (int i = 0; i < 10; ++i) fprintf(stderr, "%llu%s", h[i], i < 9 ? ", " : "], \"w15\": [");
+  for (int i = 0; i < 10; ++i) fprintf(stderr, "%llu%s", h[16 + i], i < 9 ? ", " : "]}\n");
+}
 
 WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
   WyLevel L{};
   L.q = lv.q; L.rem2 = lv.rem2; L.odd_last = lv.odd_last; L.nblocks = lv.nblocks;
   L.V = lv.V; L.ldv = lv.ldv; L.T = lv.T; L.tstride = lv.tstride;
   L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax; L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap);
+  L.trace = wy_trace_buf();
   return L;
 }
 
@@ -89,10 +110,12 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
+  const int grid = std::min(lv.nblocks, h->sms);
   cudaError_t e;
-#define UPC(U, N) wy_up_t<U, N>(L, P, C, s, smem, h->stream)
+#define UPC(U, N) wy_up_t<U, N>(L, P, C, s, grid, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, UPC)
 #undef UPC
+  wy_trace_dump("up", L, h->stream);
   ++h->st.kernel_launches;
   if (e != cudaSuccess) {
     fprintf(stderr, "[pqr] tsqr up launch: %s\n", cudaGetErrorString(e));
@@ -106,13 +129,16 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
   TsqrState* ts = h->ts;
   WyLevel L = to_wy(ts, lv);
   L.cin = cin; L.ldci = ldci; L.Y = Y; L.ldy = ldy;
+  L.yvec = ((ldy & 1) == 0 && aligned16(Y)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = ncol > 8 ? 2 : 1;
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
+  const int grid = std::min(lv.nblocks, h->sms);
   cudaError_t e;
-#define DNC(U, N) wy_down_t<U, N>(L, P, Call, t, ncol, smem, h->stream)
+#define DNC(U, N) wy_down_t<U, N>(L, P, Call, t, ncol, grid, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, DNC)
 #undef DNC
+  wy_trace_dump("down", L, h->stream);
   ++h->st.kernel_launches;
   if (e != cudaSuccess) {
     fprintf(stderr, "[pqr] tsqr down launch: %s\n", cudaGetErrorString(e));
@@ -228,6 +254,7 @@ int alloc_level(Ctx* h, TsqrLv& lv, int wmax, bool with_io) {
   if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || wy_smem(lv.RP, wmax, ts->cap, 2) > (size_t)kSmemBudget) return PQR_EPLAN;
   lv.tstride = (int64_t)16 * ts->cap;
   if (lv.owns_v && (rc = dalloc(&lv.V, (size_t)lv.rows * ts->cap))) return rc;
+  if (lv.owns_v && with_io) CUDA_TRY(cudaMemsetAsync(lv.V, 0, sizeof(double) * lv.rows * ts->cap, h->stream));
   if ((rc = dalloc(&lv.T, (size_t)lv.nblocks * lv.tstride))) return rc;
   if (with_io) {
     if ((rc = dalloc(&lv.in, (size_t)lv.rows * wmax)) || (rc = dalloc(&lv.dn, (size_t)lv.rows * wmax))) return rc;
@@ -263,6 +290,8 @@ int tsqr_alloc(Ctx* h) {
   ts->nb = nb;
   int rc;
   TRY(alloc_level(h, leaf, wmax, false));
+  if (n & 1)  // zero pad row n of every reflector column (bulk copies of the odd last block read it)
+    CUDA_TRY(cudaMemset2DAsync(leaf.V + n, leaf.ldv * sizeof(double), 0, sizeof(double), cap, h->stream));
   ts->lv.clear();
   ts->lv.push_back(leaf);
   int pl = (int)p0;
@@ -310,6 +339,14 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
   h->k = 0;
   ts->C = 0;
   const int chunk = ts->wmax;
+  double* Qal = nullptr;  // 16-byte aligned copy with even ld for the bulk copies
+  if (k > 0 && ((ldq & 1) || !aligned16(Q))) {
+    TRY(dalloc(&Qal, (size_t)h->ld * k));
+    CUDA_TRY(cudaMemcpy2DAsync(Qal, h->ld * sizeof(double), Q, ldq * sizeof(double),
+                               h->cfg.n_local * sizeof(double), k, cudaMemcpyDeviceToDevice, h->stream));
+    Q = Qal;
+    ldq = h->ld;
+  }
   for (int c0 = 0; c0 < k; c0 += chunk) {
     const int cs = std::min(chunk, k - c0);
     TRY(tsqr_up_sweep(h, Q + (int64_t)c0 * ldq, ldq, cs));
@@ -317,6 +354,10 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
     TRY(tsqr_stage_panel(h, cs));
     TRY(tsqr_commit(h, cs, cs));
     h->k += cs;
+  }
+  if (Qal) {
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    cudaFree(Qal);
   }
   return PQR_OK;
 }
@@ -326,6 +367,13 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
   TsqrState* ts = h->ts;
   if (ts->C + s > ts->cap) return PQR_ECAPACITY;
   const int np = (int)ts->panels.size();
+  if ((ldx & 1) || !aligned16(X)) {  // the leaf kernel streams X with 16-byte bulk copies
+    if (!h->stageX && dalloc(&h->stageX, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
+    CUDA_TRY(cudaMemcpy2DAsync(h->stageX, h->ld * sizeof(double), X, ldx * sizeof(double),
+                               h->cfg.n_local * sizeof(double), s, cudaMemcpyDeviceToDevice, h->stream));
+    X = h->stageX;
+    ldx = h->ld;
+  }
   TRY(tsqr_up_sweep(h, X, ldx, s));
   TRY(run_top(h, s, false, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
   TRY(tsqr_stage_panel(h, s));

@@ -1,49 +1,65 @@
-// tsqr_wy.cuh — TreeTSPQR level kernels with blocked (compact-WY) reflector panels and
-// fp64 MMAs (§4.1 Alg. 9 with Householder local/reduction subalgorithms).
+// tsqr_wy.cuh — TreeTSPQR level kernels (§4.1 Alg. 9 with Householder local and
+// reduction subalgorithms), persistent, with blocked (compact-WY) reflector panels and
+// fp64 MMAs (mma.sync m8n8k4 .f64, SASS DMMA).
 //
-// A level block holds R <= 256*UW rows; warp w (of 16) owns UW units of 16
-// rows, lane (g = l>>2, q = l&3) keeping rows 16u+4q+{0..3} of columns 8nt+g in
-// registers (the D-fragment layout of the update MMA below).  The block's reflectors
-// are grouped in panels (the reflectors created by one call, or one LOR-build chunk):
-// H_a ... H_b = I - V T V^T with T^{-1} = I/2 + striu(V^T V) (unit-norm v, Eq. (hh)).
+// Blocks of a level (leaf row blocks, or tree nodes) are processed by a persistent grid
+// (one 512-thread CTA per SM, CTA i takes blocks i, i + grid, ...).  A block holds
+// R <= 256*UW rows; warp w (of 16) owns UW units of 16 rows, lane (g = l>>2, q = l&3)
+// keeping rows 16u+4q+{0..3} of columns 8nt+g in registers (the D-fragment layout of the
+// update MMA below).  The block's reflectors are grouped in panels (the s reflectors one
+// call creates, or one LOR-build chunk): H_a ... H_b = I - V T V^T with
+// T^{-1} = I/2 + striu(V^T V) (unit-norm v, Eq. (hh)).
 //
 //   stage 1 (Q_b^T X):  for each panel in order   Z = V^T X, Z' = T^T Z, X -= V Z'
 //   stage 2 (Q_b Y):    for each panel reversed    Z = V^T Y, Z' = T Z,   Y -= V Z'
 //
-// Z = V^T X is an m8n8k4 DMMA Gram (K = rows: lane q supplies rows 4q..4q+3 as four
-// k-steps); X -= V Z' is X^T -= Z'^T V^T (K = panel columns, N = rows, the even/odd
-// row trick of the update kernel).  Panels are double-buffered in shared memory with
-// cp.async; the panel stride RP = 10 (mod 16) doubles makes both fragment patterns
-// bank-conflict-free (the update k-steps take columns 2q+kk so the four columns of an
-// LDS.128 phase land in four distinct 32-byte bank groups).
+// Memory: everything a block streams (its X — stage 1 only — and every panel V with its
+// T) is a "ring item", copied by cp.async.bulk into one of nbuf shared-memory slots and
+// completed on that slot's mbarrier.  One producer lane keeps nbuf items in flight
+// across block boundaries, so the next block's data lands while this block does its
+// Householder tail; a slot is refilled only after the block-wide barrier that proves
+// every warp has finished the item it held.
 //
-// After the committed panels, stage 1 factors rows C..R-1 of the s new columns with
-// Householder reflectors (Alg. 6 lines 2-9; never deflating, reading R4), stores them
-// (rows < pivot zeroed) and the panel's T, and writes [P_b; N_b] to the parent slot.
+// Per panel: Gram Z = V^T x (per-warp DMMA partials) -> barrier -> fixed-order sum of
+// the 16 partials by |Z| threads -> barrier -> every warp forms Z'^T = Z^T T (or Z^T T^T)
+// with two DMMAs from shared memory -> update x^T -= Z'^T V^T.  Two barriers per panel.
+//
+// Stage-1 tail (Alg. 6 lines 2-9 on rows C..R-1 of the s new columns; never deflating,
+// reading R4): the columns stay in registers.  Round c makes one block-wide reduction of
+// D_c' = x_c . x_c' over rows >= r = C+c for all c' >= c (c' = c gives lambda^2) and
+// broadcasts row r; then every lane knows the reflector
+//   v = (x_c - sigma*lambda e_r) / sqrt(2 lambda (lambda + |x_c[r]|)),  sigma = -sgn(x_c[r]),
+// and v . x_c' = (D_c' - sigma*lambda x_c'[r]) / sqrt(...), so one barrier per column.
+// Then T of the new panel from V^T V (one more reduction), and the outputs.
 #pragma once
 #include "common.cuh"
 
 namespace pqr {
 
 constexpr int kWyWarps = 16;
-constexpr int kWyThreads = 32 * kWyWarps;
+constexpr int kWyThreads = 32 * kWyWarps;       // consumer threads
+constexpr int kWyLaunch = kWyThreads + 32;       // + one producer warp
 constexpr int kWyRowsPerUW = 16 * kWyWarps;  // block rows covered per unit-per-warp
-constexpr int kWyMaxW = 16;  // widest panel
+constexpr int kWyMaxW = 16;                  // widest panel
+constexpr int kWyHH = 2 * (kWyWarps * 16 + 16);  // Householder-round reduction buffers
 
 struct WyLevel {
   int64_t q, rem2;      // block b: q + 2*(b < rem2) rows starting at b*q + 2*min(b, rem2) (even);
   int odd_last;         // ... the last block has one more row when the level's row count is odd
   int nblocks;
-  const double* X; int64_t ldx;     // stage-1 input (level rows)
-  double* V; int64_t ldv;           // reflectors (level rows); column j = reflector j
+  const double* X; int64_t ldx;     // stage-1 input (level rows); 16-B aligned, ldx even
+  double* V; int64_t ldv;           // reflectors (level rows); column j = reflector j; ldv even,
+                                    // and row R of an odd-sized last block is a zero pad row
   double* T; int64_t tstride;       // block b's T area at T + b*tstride; panel at +16*start
   double* out; int64_t ldo;         // stage-1 output: block b -> rows b*cap ...
   const double* cin; int64_t ldci;  // stage-2 coefficients: block b -> rows b*cap ...
   double* Y; int64_t ldy;           // stage-2 output (level rows)
+  int yvec;                         // Y 16-B aligned with even ldy (paired stores)
   int cap;
-  int RP;                           // smem panel stride (>= max block rows, = 10 mod 16)
-  int wmax;                         // widest panel (<= 16) -> smem panel buffer width
-  int nbuf;                         // panel buffers (2 or 3)
+  int RP;                           // smem panel stride (>= max block rows + 1, = 10 mod 16)
+  int wmax;                         // widest panel (<= 16) -> smem slot width
+  int nbuf;                         // ring slots (>= 2)
+  unsigned long long* trace;        // optional phase-cycle counters (tools; nullptr = off)
 };
 
 struct WyPanels {
@@ -56,429 +72,470 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
   return (int)(L.q + (b < L.rem2 ? 2 : 0) + (b == L.nblocks - 1 ? L.odd_last : 0));
 }
 
-// column of the update k-step kk for lane quarter q (conflict-free pattern, see header)
-PQR_DEV int wy_col(int kk, int q) { return 8 * (kk >> 1) + 2 * q + (kk & 1); }
-
-// Stage panel (start, w) of this block into buf (RP x w8 col-major); rows R..kWyRowsPerUW*UW-1
-// and columns w..w8-1 are zero-filled (they meet zero rows / zero coefficients in the MMAs).
-template <int UW>
-PQR_DEV void wy_load_panel(double* buf, const WyLevel& L, int64_t r0, int R, int start, int w, int RP) {
-  constexpr int pairs = kWyRowsPerUW * UW / 2;
-  const int w8 = (w + 7) & ~7;
-  for (int e = threadIdx.x; e < w8 * pairs; e += kWyThreads) {
-    const int j = e / pairs, p = e - j * pairs;
-    const int row = 2 * p;
-    const double* src = L.V + (int64_t)(start + j) * L.ldv + r0 + row;
-    const int bytes = (j < w && row < R) ? (row + 1 < R ? 16 : 8) : 0;
-    cp_async16(buf + j * RP + row, bytes ? (const void*)src : (const void*)L.V, bytes);
-  }
+// shared-memory bytes of a level kernel (host and device agree on this layout)
+inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
+  const size_t E = (size_t)wmax * wmax;
+  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 256) * sizeof(double) +
+         (size_t)((cap + 2) & ~1) * sizeof(int2) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
-// Block-wide: Z (w8 x s8, smem, col-major ld 16) = sum over warps of the D fragments
-// acc[mt][nt][2]; red is kWyWarps*256 doubles.  Ends with a __syncthreads.
-template <int NT>
-PQR_DEV void wy_reduce_Z(double (&acc)[2][NT][2], int mtn, double* red, double* Z, int wm) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, q = lane & 3;
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int i = 8 * mt + g, c = 8 * nt + 2 * q + v;
-        if (i < wm && c < wm) red[warp * wm * wm + i + wm * c] = (mt < mtn) ? acc[mt][nt][v] : 0.0;
-      }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 256; e += kWyThreads) {
-    const int i = e & 15, c = e >> 4;
-    double a = 0.0;
-    if (i < wm && c < wm) {
-#pragma unroll
-      for (int w = 0; w < kWyWarps; ++w) a += red[w * wm * wm + i + wm * c];
-    }
-    Z[e] = a;
-  }
-  __syncthreads();
-}
+template <int UW, int NT, bool UP>
+PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol) {
+  extern __shared__ __align__(16) double sm[];
+  const int RP = L.RP, wm = L.wmax, nbuf = L.nbuf;
+  const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
+  const int E = wm * wm;
+  double* ring = sm;
+  double* red = ring + (size_t)nbuf * SS;  // E x (kWyWarps + 1): per-warp partials, entry-major (padded)
+  double* Zs = red + (kWyWarps + 1) * E;   // E: reduced Z (ld wm)
+  double* hred = Zs + E;                   // 2 x (kWyWarps*16 partials + 16 pivot-row values)
+  double* diagv = hred + kWyHH;            // 16: sigma*lambda of the new columns
+  double* tsc = diagv + 16;                // 16 x 16: back-substitution scratch of the T columns
+  int2* pans = reinterpret_cast<int2*>(tsc + 256);
+  uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));
+  uint64_t* empty = full + nbuf;
 
-// apply one panel (in smem `vb`, width w) to the register block x:
-//   x <- x - V (Tp Z),  Z = V^T x,  Tp = T^T (stage 1) or T (stage 2);  Tg in smem (ld w)
-template <int UW, int NT>
-PQR_DEV void wy_apply_panel(double (&x)[UW][NT][4], const double* vb, const double* Tg, int w, bool transT,
-                            int RP, double* red, double* Zp, int wm) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  const int mtn = (w + 7) >> 3;
-  // ---- Z = V^T x (per-warp partials; two accumulator chains over alternate units) ----
-  double acc[2][2][NT][2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    if (mt < mtn) {
-#pragma unroll
-      for (int u = 0; u < UW; ++u) {
-        const int row = 16 * (warp * UW + u) + 4 * q;
-        const double* vp = vb + (8 * mt + g) * RP + row;
-        const double2 a01 = *reinterpret_cast<const double2*>(vp);
-        const double2 a23 = *reinterpret_cast<const double2*>(vp + 2);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          double (&ac)[2] = acc[u & 1][mt][nt];
-          dmma884(ac[0], ac[1], a01.x, x[u][nt][0]);
-          dmma884(ac[0], ac[1], a01.y, x[u][nt][1]);
-          dmma884(ac[0], ac[1], a23.x, x[u][nt][2]);
-          dmma884(ac[0], ac[1], a23.y, x[u][nt][3]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int i = 8 * mt + g, c = 8 * nt + 2 * q + v;
-        if (i < wm && c < wm) red[warp * wm * wm + i + wm * c] = (mt < mtn) ? acc[0][mt][nt][v] + acc[1][mt][nt][v] : 0.0;
-      }
-  __syncthreads();
-  // ---- Z = sum over warps of red (fixed order), then Z' = T^T Z (stage 1) or T Z (stage 2) ----
-  const int E = wm * wm;
-  double* Zs = red + kWyWarps * E;  // E doubles after the per-warp partials
-  if (tid < E) {
-    double z = 0.0;
-#pragma unroll
-    for (int ww = 0; ww < kWyWarps; ++ww) z += red[ww * E + tid];
-    Zs[tid] = z;
-  }
-  __syncthreads();
-  if (tid < 256) {
-    const int i = tid & 15, c = tid >> 4;
-    double a = 0.0;
-    if (i < w && c < wm) {
-      if (transT) {
-        for (int l = 0; l <= i; ++l) a += Tg[l + i * w] * Zs[l + wm * c];
-      } else {
-        for (int l = i; l < w; ++l) a += Tg[i + l * w] * Zs[l + wm * c];
-      }
-    }
-    Zp[tid] = a;
-  }
-  __syncthreads();
-  // ---- x^T -= Z'^T V^T ----
-  const int kks = 2 * mtn;
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
-    if (kk < kks) {
-      const int j = wy_col(kk, q);
-      double am[NT];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) am[nt] = -Zp[j + 16 * (8 * nt + g)];
-#pragma unroll
-      for (int u = 0; u < UW; ++u) {
-        const int row = 16 * (warp * UW + u) + 2 * g;
-        const double2 bv = *reinterpret_cast<const double2*>(vb + j * RP + row);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          dmma884(x[u][nt][0], x[u][nt][2], am[nt], bv.x);  // even rows 4q, 4q+2
-          dmma884(x[u][nt][1], x[u][nt][3], am[nt], bv.y);  // odd rows 4q+1, 4q+3
-        }
-      }
-    }
-  }
-}
-
-// Apply the first np panels, forward (stage 1, H_0 first, T^T) or reversed (stage 2, T).
-// Panels (and each panel's T, w x w) stream through L.nbuf shared-memory buffers: one
-// thread issues one cp.async.bulk per panel column (R rows, contiguous in HBM: 8 KB at
-// R = 1024, long enough for the bulk-copy engine) plus one for T, completing on the
-// buffer's mbarrier; while panel i is applied, panels i+1 .. i+nbuf-1 are in flight.
-// Rows R..(256*UW)-1 and columns w..w8-1 of every buffer are zeroed once (never copied).
-template <int UW, int NT>
-PQR_DEV void wy_apply_panels(double (&x)[UW][NT][4], const WyLevel& L, const WyPanels& P, int64_t b, int64_t r0,
-                             int R, bool forward, double* vbuf, double* red, double* Zp, int2* pans,
-                             uint64_t* full) {
   const int np = P.np;
-  if (np == 0) return;
-  const int RP = L.RP, nbuf = L.nbuf, wm = L.wmax;
-  const int bstride = RP * wm + 256;  // panel + its T
-  const int Reven = R & ~1;           // rows moved by the bulk copies
-  for (int i = threadIdx.x; i < np; i += kWyThreads) pans[i] = P.pan[i];
-  // zero the never-copied parts: rows >= Reven of every column (row R-1 of an odd block is
-  // loaded per element below), all rows of columns >= w are zeroed per panel if w < w8
-  for (int e = threadIdx.x; e < nbuf * wm * (RP - Reven); e += kWyThreads) {
-    const int bb = e / (wm * (RP - Reven)), rem = e % (wm * (RP - Reven));
-    const int j = rem / (RP - Reven), row = Reven + rem % (RP - Reven);
-    vbuf[bb * bstride + j * RP + row] = 0.0;
-  }
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < nbuf; ++i) mbar_init(&full[i], 1);
+  const int ipb = np + (UP ? 1 : 0);  // ring items per block (stage 1: X first)
+  const int64_t nbl = L.nblocks;
+  const int nb_cta = (int64_t)blockIdx.x < nbl ? (int)((nbl - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int64_t total = (int64_t)nb_cta * ipb;
+
+  // never-copied slot parts must hold finite values (they meet zero coefficients)
+  for (int e = tid; e < nbuf * SS; e += kWyLaunch) ring[e] = 0.0;
+  for (int i = tid; i < np; i += kWyLaunch) pans[i] = P.pan[i];
+  if (tid == 0) {
+    for (int i = 0; i < nbuf; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kWyWarps);
+    }
     fence_mbar_init();
   }
   fence_proxy_async_smem();
-  const double* Tb = L.T + b * L.tstride;
   __syncthreads();
-  auto pidx = [&](int i) { return forward ? i : np - 1 - i; };
-  auto issue = [&](int i) {  // thread 0 only
-    if (i < np) {
-      const int2 pn = pans[pidx(i)];
-      double* buf = vbuf + (i % nbuf) * bstride;
-      uint64_t* bar = &full[i % nbuf];
-      const uint32_t tbytes = (uint32_t)((pn.y * pn.y + 1) & ~1) * 8u;
-      mbar_arrive_expect_tx(bar, (uint32_t)pn.y * Reven * 8u + tbytes);
-      for (int j = 0; j < pn.y; ++j)
-        bulk_g2s(buf + j * RP, L.V + (int64_t)(pn.x + j) * L.ldv + r0, (uint32_t)Reven * 8u, bar);
-      bulk_g2s(buf + RP * wm, Tb + 16 * pn.x, tbytes, bar);
+
+  // ---- producer warp: streams ring item `it` into slot it % nbuf once the consumers have
+  // released the slot's previous item (empty barrier, one arrival per consumer warp) ----
+  if (warp == kWyWarps) {
+    if (lane == 0) {
+      for (int it = 0; it < total; ++it) {
+        const int jb = it / ipb;
+        const int p = it - jb * ipb;
+        const int slot = it % nbuf;
+        if (it >= nbuf) mbar_wait(&empty[slot], (uint32_t)((it / nbuf - 1) & 1));
+        const int64_t b = blockIdx.x + (int64_t)jb * gridDim.x;
+        const int64_t r0 = wy_start(L, b);
+        const int R = wy_rows(L, b);
+        double* buf = ring + (size_t)slot * SS;
+        uint64_t* bar = &full[slot];
+        if (UP && p == 0) {
+          const int Re = R & ~1;  // an odd last row is read from global by the consumer
+          mbar_arrive_expect_tx(bar, (uint32_t)(s * Re * 8));
+          if (Re)
+            for (int c = 0; c < s; ++c)
+              bulk_g2s(buf + c * RP, L.X + r0 + (int64_t)c * L.ldx, (uint32_t)Re * 8u, bar);
+        } else {
+          const int2 pn = pans[UP ? p - 1 : np - 1 - p];
+          const int Rc = R + (R & 1);  // includes the zero pad row of an odd block
+          const uint32_t tb = (uint32_t)((pn.y * pn.y + 1) & ~1) * 8u;
+          mbar_arrive_expect_tx(bar, (uint32_t)pn.y * Rc * 8u + tb);
+          for (int j = 0; j < pn.y; ++j)
+            bulk_g2s(buf + j * RP, L.V + (int64_t)(pn.x + j) * L.ldv + r0, (uint32_t)Rc * 8u, bar);
+          bulk_g2s(buf + RP * wm, L.T + b * L.tstride + 16 * pn.x, tb, bar);
+        }
+      }
     }
+    return;
+  }
+  // consumer warps only from here: named barrier 1 over the kWyThreads consumer threads
+  auto cbar = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(kWyThreads) : "memory"); };
+  // this warp is done with ring item `it` (all of its lanes' reads precede the arrival)
+  auto release = [&](int64_t it) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[it % nbuf]);
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < nbuf - 1; ++i) issue(i);
-  for (int i = 0; i < np; ++i) {
-    const int2 pc = pans[pidx(i)];
-    double* buf = vbuf + (i % nbuf) * bstride;
-    // per-element pieces: the odd last row, and zero columns w..w8-1 (stale from a wider panel)
-    if (R & 1)
-      for (int j = threadIdx.x; j < pc.y; j += kWyThreads) buf[j * RP + R - 1] = L.V[(int64_t)(pc.x + j) * L.ldv + r0 + R - 1];
-    const int w8 = (pc.y + 7) & ~7;
-    for (int e = threadIdx.x; e < (w8 - pc.y) * Reven; e += kWyThreads) buf[(pc.y + e / Reven) * RP + e % Reven] = 0.0;
-    fence_proxy_async_smem();  // order these generic writes before later bulk copies into the buffer
-    mbar_wait(&full[i % nbuf], (uint32_t)(i / nbuf) & 1u);
-    __syncthreads();          // panel i complete and visible; every warp is done with panel i-1
-    if (threadIdx.x == 0) issue(i + nbuf - 1);  // refill the buffer panel i-1 used
-    wy_apply_panel<UW, NT>(x, buf, buf + RP * wm, pc.y, forward, RP, red, Zp, wm);
-  }
-  __syncthreads();
-}
-
-// ----------------------------------------------------------------------------
-// stage 1
-// ----------------------------------------------------------------------------
-template <int UW, int NT>
-__global__ void __launch_bounds__(kWyThreads, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s) {
-  extern __shared__ __align__(16) double sm[];
-  const int RP = L.RP;
-  double* vbuf = sm;                                   // nbuf x (RP x wmax + 256)
-  double* red = vbuf + L.nbuf * (RP * L.wmax + 256);   // (kWyWarps + 1) x wmax^2
-  double* Z = red + (kWyWarps + 1) * L.wmax * L.wmax;  // 256
-  double* Zp = Z + 256;                                // 256
-  double* bc = Zp + 256;                               // 64 scratch
-  int2* pans = reinterpret_cast<int2*>(bc + 64);       // panel list (cap + 1)
-  uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));  // nbuf mbarriers
-  double* Vn = vbuf;                                   // RP x s8: the new reflectors (aliases the
-                                                       // panel buffers, free after the panels)
-  const int64_t b = blockIdx.x;
-  const int64_t r0 = wy_start(L, b);
-  const int R = wy_rows(L, b);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, q = lane & 3;
-
-  double x[UW][NT][4];
-#pragma unroll
-  for (int u = 0; u < UW; ++u)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
-        x[u][nt][i] = (row < R && c < s) ? L.X[r0 + row + (int64_t)c * L.ldx] : 0.0;
-      }
-  wy_apply_panels<UW, NT>(x, L, P, b, r0, R, true, vbuf, red, Zp, pans, full);
-
-  // ---- Householder QR of rows C..R-1 of the s new columns (Alg. 6 lines 2-9) ----
-  // The block is moved from the MMA register layout to shared memory (xs, column-major),
-  // where thread t owns rows t, t+512, ...: every thread takes part in each column's
-  // reductions.  Two block barriers per column: red1 carries column c's norm partials
-  // (written right after column c's last update), red2 the dot products of v_c with the
-  // later columns; the buffers alternate, so no third barrier is needed.
-  const int s8 = (s + 7) & ~7;
-  double* xs = vbuf + RP * s8;   // RP x s8 (Vn = vbuf holds the new reflectors)
-  __syncthreads();
-  for (int e = tid; e < RP * s8; e += kWyThreads) Vn[e] = 0.0;
-#pragma unroll
-  for (int u = 0; u < UW; ++u)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
-        if (c < s8) xs[c * RP + row] = x[u][nt][i];
-      }
-  constexpr int RPT = (kWyRowsPerUW * UW + kWyThreads - 1) / kWyThreads;  // rows per thread
-  double* red1 = red;          // kWyWarps
-  double* red2 = red + 64;     // kWyWarps x 16
-  auto norm_partial = [&](int c) {
-    const int r = C + c;
-    double part = 0.0;
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int row = tid + j * kWyThreads;
-      if (row >= r && row < R) part += xs[c * RP + row] * xs[c * RP + row];
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (lane == 0) red1[warp] = part;
+  // fixed-order sum of the kWyWarps partials: G = kWyThreads / E threads per entry;
+  // partials are entry-major with stride kWyWarps + 1 (conflict-free for writers and readers)
+  auto reduce_Z = [&]() {
+    const int G = kWyThreads / E;
+    const int e = tid / G, part = tid - e * G;
+    double z = 0.0;
+    for (int ww = part; ww < kWyWarps; ww += G) z += red[e * (kWyWarps + 1) + ww];
+    for (int o = 1; o < G; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (part == 0) Zs[e] = z;
   };
-  __syncthreads();
-  if (s > 0) norm_partial(0);
-  for (int c = 0; c < s; ++c) {
-    const int r = C + c;
-    __syncthreads();  // S1: norm partials of column c in red1; column c final above row r
-    double lam2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < kWyWarps; ++w) lam2 += red1[w];
-    const double lam = sqrt(lam2);
-    const double u0 = r < R ? xs[c * RP + r] : 0.0;
-    const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
-    const double diag = sigma * lam;
-    const double nv2 = 2.0 * lam * (lam + fabs(u0));
-    const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lam == 0 (R4)
-    double v[RPT];
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int row = tid + j * kWyThreads;
-      const double xv = row < R ? xs[c * RP + row] : 0.0;
-      v[j] = (row > r && row < R) ? xv * inv : (row == r ? (xv - diag) * inv : 0.0);
-    }
-    // dot products v . x[:, c'] for c' > c (reduced over the warp, then over warps)
-    for (int cc = c + 1; cc < s; ++cc) {
-      double a = 0.0;
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int row = tid + j * kWyThreads;
-        if (row < R) a += v[j] * xs[cc * RP + row];
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      if (lane == 0) red2[warp * 16 + cc] = a;
-    }
-    __syncthreads();  // S2: dots in red2; every thread has read u0 and red1
-#pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-      const int row = tid + j * kWyThreads;
-      if (row < R) {
-        Vn[c * RP + row] = v[j];
-        if (row >= r) xs[c * RP + row] = (row == r) ? diag : 0.0;
-      }
-    }
-    for (int cc = c + 1; cc < s; ++cc) {
-      double d = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWyWarps; ++w) d += red2[w * 16 + cc];
-      const double f = 2.0 * d;
-#pragma unroll
-      for (int j = 0; j < RPT; ++j) {
-        const int row = tid + j * kWyThreads;
-        if (row < R) xs[cc * RP + row] -= f * v[j];
-      }
-    }
-    if (c + 1 < s) norm_partial(c + 1);
+  // optional phase tracing (CTA 0, warps 0 and 15, lane 0): cycles per phase in smem
+  __shared__ unsigned long long s_tr[2][16];
+  const bool tr_on = L.trace != nullptr && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kWyWarps - 1);
+  const int tr_w = warp == 0 ? 0 : 1;
+  long long tr_t0 = 0;
+  if (tr_on) {
+    for (int i = 0; i < 16; ++i) s_tr[tr_w][i] = 0;
+    tr_t0 = clock64();
   }
-  __syncthreads();
+#define WY_TR(k)                                       \
+  if (tr_on) {                                         \
+    const long long t1_ = clock64();                   \
+    s_tr[tr_w][k] += (unsigned long long)(t1_ - tr_t0); \
+    tr_t0 = t1_;                                       \
+  }
 
-  // ---- outputs: [P_b; N_b] = rows 0..C+s-1, the new reflectors, the new panel's T ----
-  double* outb = L.out + b * L.cap;
-  for (int e = tid; e < s * (C + s); e += kWyThreads) {
-    const int c = e / (C + s), row = e - c * (C + s);
-    if (row < R) outb[row + (int64_t)c * L.ldo] = xs[c * RP + row];
-  }
-  for (int e = tid; e < s * R; e += kWyThreads) {
-    const int c = e / R, row = e - c * R;
-    L.V[r0 + row + (int64_t)(C + c) * L.ldv] = Vn[c * RP + row];
-  }
-  // V^T V of the new panel: Gram MMA from smem Vn (same fragment pattern as Z = V^T x)
-  {
-    double acc[2][2][2];
+  int64_t it = 0;  // consumer item cursor
+  int hpar = 0;    // Householder-round buffer parity
+  for (int jb = 0; jb < nb_cta; ++jb) {
+    const int64_t b = blockIdx.x + (int64_t)jb * gridDim.x;
+    const int64_t r0 = wy_start(L, b);
+    const int R = wy_rows(L, b);
+    const bool mrow = kWyRowsPerUW / kWyWarps * UW * (warp + 1) > R;  // warp holds rows >= R
+    double x[UW][NT][4];
+    if (UP) {
+      WY_TR(9);
+      mbar_wait(&full[it % nbuf], (uint32_t)((it / nbuf) & 1));
+      WY_TR(0);
+      const double* buf = ring + (size_t)(it % nbuf) * SS;
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+      for (int u = 0; u < UW; ++u)
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const int mtn = (s + 7) >> 3;
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-    for (int u = 0; u < UW; ++u) {
-      const int row = 16 * (warp * UW + u) + 4 * q;
+          for (int i = 0; i < 4; ++i) {
+            const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+            double v = 0.0;
+            if (c < s && row < R)
+              v = (row == R - 1 && (R & 1)) ? L.X[r0 + row + (int64_t)c * L.ldx] : buf[c * RP + row];
+            x[u][nt][i] = v;
+          }
+      release(it);
+      ++it;
+    } else {
+      const double* cb = L.cin + b * L.cap;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        if (nt < mtn) {
-          const double2 b01 = *reinterpret_cast<const double2*>(Vn + (8 * nt + g) * RP + row);
-          const double2 b23 = *reinterpret_cast<const double2*>(Vn + (8 * nt + g) * RP + row + 2);
+      for (int u = 0; u < UW; ++u)
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            if (mt < mtn) {
-              const double2 a01 = *reinterpret_cast<const double2*>(Vn + (8 * mt + g) * RP + row);
-              const double2 a23 = *reinterpret_cast<const double2*>(Vn + (8 * mt + g) * RP + row + 2);
-              dmma884(acc[mt][nt][0], acc[mt][nt][1], a01.x, b01.x);
-              dmma884(acc[mt][nt][0], acc[mt][nt][1], a01.y, b01.y);
-              dmma884(acc[mt][nt][0], acc[mt][nt][1], a23.x, b23.x);
-              dmma884(acc[mt][nt][0], acc[mt][nt][1], a23.y, b23.y);
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+            x[u][nt][i] = (row < Call && row < R && c < s) ? cb[row + (int64_t)c * L.ldci] : 0.0;
+          }
+    }
+
+    // ---------------- committed panels ----------------
+    for (int p = 0; p < np; ++p, ++it) {
+      WY_TR(9);
+      mbar_wait(&full[it % nbuf], (uint32_t)((it / nbuf) & 1));
+      WY_TR(0);
+      const double* vb = ring + (size_t)(it % nbuf) * SS;
+      const double* Tg = vb + RP * wm;
+      const int w = pans[UP ? p : np - 1 - p].y;
+      const int mtn = (w + 7) >> 3;
+      // Z = V^T x: per-warp partials, two accumulator chains over alternate units
+      double acc[2][2][NT][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt < mtn) {
+#pragma unroll
+          for (int u = 0; u < UW; ++u) {
+            const int row = 16 * (warp * UW + u) + 4 * q;
+            const double* vp = vb + (8 * mt + g) * RP + row;
+            const double2 a01 = *reinterpret_cast<const double2*>(vp);
+            const double2 a23 = *reinterpret_cast<const double2*>(vp + 2);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              double (&ac)[2] = acc[u & 1][mt][nt];
+              dmma884(ac[0], ac[1], a01.x, x[u][nt][0]);
+              dmma884(ac[0], ac[1], a01.y, x[u][nt][1]);
+              dmma884(ac[0], ac[1], a23.x, x[u][nt][2]);
+              dmma884(ac[0], ac[1], a23.y, x[u][nt][3]);
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              red[((8 * mt + g) + wm * (8 * nt + 2 * q + v)) * (kWyWarps + 1) + warp] = acc[0][mt][nt][v] + acc[1][mt][nt][v];
+        }
+      }
+      WY_TR(1);
+      cbar();  // B1: partials complete; every warp is done with the previous item
+      WY_TR(2);
+      WY_TR(3);
+      reduce_Z();
+      WY_TR(4);
+      cbar();  // B2: Z complete
+      WY_TR(5);
+      // Z'^T = Z^T T (stage 1) or Z^T T^T (stage 2): lane gets Z'[8jt+2q+v][8nt+g]
+      double zp[NT][2][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int jt = 0; jt < 2; ++jt) {
+          zp[nt][jt][0] = zp[nt][jt][1] = 0.0;
+          if (jt < mtn) {
+            const int jj = 8 * jt + g;
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              if (k4 < 2 * mtn) {
+                const int l = 4 * k4 + q;
+                const double a = Zs[l + wm * (8 * nt + g)];
+                const double bt = (l < w && jj < w) ? (UP ? Tg[l + w * jj] : Tg[jj + w * l]) : 0.0;
+                dmma884(zp[nt][jt][0], zp[nt][jt][1], a, bt);
+              }
+            }
+          }
+        }
+      // x^T -= Z'^T V^T
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (kk < 2 * mtn) {
+          const int j = 8 * (kk >> 1) + 2 * q + (kk & 1);
+          double am[NT];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) am[nt] = -zp[nt][kk >> 1][kk & 1];
+#pragma unroll
+          for (int u = 0; u < UW; ++u) {
+            const int row = 16 * (warp * UW + u) + 2 * g;
+            const double2 bv = *reinterpret_cast<const double2*>(vb + j * RP + row);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              dmma884(x[u][nt][0], x[u][nt][2], am[nt], bv.x);  // even rows 4q, 4q+2
+              dmma884(x[u][nt][1], x[u][nt][3], am[nt], bv.y);  // odd rows 4q+1, 4q+3
             }
           }
         }
       }
-    }
-    wy_reduce_Z<2>(acc, mtn, red, Z, L.wmax);  // Z = V^T V (16 x 16, ld 16)
-    // T^{-1} = I/2 + striu(V^T V);  T = its inverse (upper triangular), column c by lane c
-    double* Tn = L.T + b * L.tstride + 16 * C;
-    if (tid < s) {
-      const int c = tid;
-      double col[kWyMaxW];
+      release(it);
+      WY_TR(6);
+      if (mrow) {  // rows >= R stay zero (stale slot rows may be non-zero)
 #pragma unroll
-      for (int i = 0; i < kWyMaxW; ++i) col[i] = 0.0;
-      col[c] = 2.0;  // 1 / (1/2)
-      for (int i = c - 1; i >= 0; --i) {
-        double a = 0.0;
-        for (int l = i + 1; l <= c; ++l) a += Z[i + 16 * l] * col[l];
-        col[i] = -a * 2.0;
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (16 * (warp * UW + u) + 4 * q + i >= R) x[u][nt][i] = 0.0;
       }
-      for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
     }
+
+    if constexpr (!UP) {
+      // ---------------- stage-2 output: Y_b (columns >= t written as zero) ----------------
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = 8 * nt + g;
+          if (c >= ncol) continue;
+          const int row = 16 * (warp * UW + u) + 4 * q;
+          double* yp = L.Y + r0 + row + (int64_t)c * L.ldy;
+          const bool ok = c < s;
+#pragma unroll
+          for (int i = 0; i < 4; i += 2) {
+            const double v0 = ok ? x[u][nt][i] : 0.0, v1 = ok ? x[u][nt][i + 1] : 0.0;
+            if (L.yvec && row + i + 1 < R) {
+              st2(yp + i, v0, v1);
+            } else {
+              if (row + i < R) yp[i] = v0;
+              if (row + i + 1 < R) yp[i + 1] = v1;
+            }
+          }
+        }
+    } else {
+    WY_TR(9);
+    // ---------------- stage-1 tail: Householder QR of rows C..R-1 of the s new columns ----------------
+    for (int c = 0; c < s; ++c) {
+      const int r = C + c;
+      const int ntc = c >> 3, gc = c & 7;
+      const int src = gc * 4 + q;
+      double xc[UW][4];
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double v = x[u][0][i];
+          if (NT > 1 && ntc == 1) v = x[u][NT - 1][i];
+          xc[u][i] = __shfl_sync(0xffffffffu, v, src);
+        }
+      double D[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double d = 0.0;
+#pragma unroll
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (16 * (warp * UW + u) + 4 * q + i >= r) d = fma(xc[u][i], x[u][nt][i], d);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        D[nt] = d;
+      }
+      double* hb = hred + hpar * (kWyWarps * 16 + 16);
+      hpar ^= 1;
+      if (q == 0) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) hb[warp * 16 + 8 * nt + g] = D[nt];
+      }
+      {  // the owner of pivot row r broadcasts it (select chains: no dynamic register indexing)
+        bool own_r = false;
+        double xr[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) xr[nt] = 0.0;
+#pragma unroll
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool hit = 16 * (warp * UW + u) + 4 * q + i == r;
+            own_r |= hit;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) xr[nt] = hit ? x[u][nt][i] : xr[nt];
+          }
+        if (own_r) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) hb[kWyWarps * 16 + 8 * nt + g] = xr[nt];
+        }
+      }
+      cbar();
+      double lam2 = 0.0, Dg[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) Dg[nt] = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < kWyWarps; ++ww) {
+        lam2 += hb[ww * 16 + c];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) Dg[nt] += hb[ww * 16 + 8 * nt + g];
+      }
+      const double u0 = hb[kWyWarps * 16 + c];
+      const double lam = sqrt(lam2);
+      const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
+      const double diag = sigma * lam;
+      const double nv2 = 2.0 * lam * (lam + fabs(u0));
+      const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
+      double f[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int cc = 8 * nt + g;
+        f[nt] = (cc > c && cc < s) ? 2.0 * inv * (Dg[nt] - diag * hb[kWyWarps * 16 + cc]) : 0.0;
+      }
+      if (tid == 0) diagv[c] = diag;
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = 16 * (warp * UW + u) + 4 * q + i;
+          const double vv = row > r ? xc[u][i] * inv : (row == r ? (u0 - diag) * inv : 0.0);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const bool own = (nt == ntc) && (g == gc) && row >= r;
+            x[u][nt][i] = own ? vv : fma(-f[nt], vv, x[u][nt][i]);
+          }
+        }
+    }
+
+    WY_TR(7);
+    // ---------------- T of the new panel: T^{-1} = I/2 + striu(V^T V) ----------------
+    {
+      double ac[NT][NT][2];
+#pragma unroll
+      for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) ac[mt][nt][0] = ac[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = 16 * (warp * UW + u) + 4 * q + i;
+          double vr[NT];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int cc = 8 * nt + g;
+            vr[nt] = (cc < s && row >= C + cc) ? x[u][nt][i] : 0.0;
+          }
+#pragma unroll
+          for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma884(ac[mt][nt][0], ac[mt][nt][1], vr[mt], vr[nt]);
+        }
+#pragma unroll
+      for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) red[((8 * mt + g) + wm * (8 * nt + 2 * q + v)) * (kWyWarps + 1) + warp] = ac[mt][nt][v];
+      cbar();
+      reduce_Z();
+      cbar();
+      double* Tn = L.T + b * L.tstride + 16 * C;
+      if (tid < s) {  // column c of T by back substitution
+        const int c = tid;
+        double* col = tsc + 16 * c;  // own area: with no panels the next block's rounds follow
+                                     // without a barrier and reuse hred
+        for (int i = 0; i < kWyMaxW; ++i) col[i] = 0.0;
+        col[c] = 2.0;  // 1 / (1/2)
+        for (int i = c - 1; i >= 0; --i) {
+          double a = 0.0;
+          for (int l = i + 1; l <= c; ++l) a += Zs[i + wm * l] * col[l];
+          col[i] = -a * 2.0;
+        }
+        for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
+      }
+    }
+
+    WY_TR(8);
+    // ---------------- outputs: [P_b; N_b] to the parent slot, the new reflectors ----------------
+    {
+      double* outb = L.out + b * L.cap;
+      const int rmax = R < L.cap ? R : L.cap;
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int c = 8 * nt + g;
+          if (c >= s) continue;
+          const int piv = C + c;
+          const double dg = diagv[c];
+          const int row0 = 16 * (warp * UW + u) + 4 * q;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = row0 + i;
+            if (row < rmax) outb[row + (int64_t)c * L.ldo] = row < piv ? x[u][nt][i] : (row == piv ? dg : 0.0);
+          }
+          double* vp = L.V + r0 + row0 + (int64_t)(C + c) * L.ldv;
+#pragma unroll
+          for (int i = 0; i < 4; i += 2) {
+            const int row = row0 + i;
+            const double v0 = row >= piv ? x[u][nt][i] : 0.0, v1 = row + 1 >= piv ? x[u][nt][i + 1] : 0.0;
+            if (row + 1 < R) {
+              st2(vp + i, v0, v1);
+            } else if (row < R) {
+              vp[i] = v0;
+            }
+          }
+        }
+    }
+    }  // stage-1 tail
   }
+  WY_TR(9);
+  if (tr_on)
+    for (int i = 0; i < 16; ++i) L.trace[tr_w * 16 + i] = s_tr[tr_w][i];
+#undef WY_TR
 }
 
-// ----------------------------------------------------------------------------
-// stage 2: Y_b = Q_b [coef; 0]
-// ----------------------------------------------------------------------------
 template <int UW, int NT>
-__global__ void __launch_bounds__(kWyThreads, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  extern __shared__ __align__(16) double sm[];
-  const int RP = L.RP;
-  double* vbuf = sm;
-  double* red = vbuf + L.nbuf * (RP * L.wmax + 256);
-  double* Z = red + (kWyWarps + 1) * L.wmax * L.wmax;
-  double* Zp = Z + 256;
-  int2* pans = reinterpret_cast<int2*>(Zp + 256 + 64);
-  uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));
-  const int64_t b = blockIdx.x;
-  const int64_t r0 = wy_start(L, b);
-  const int R = wy_rows(L, b);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, q = lane & 3;
-  const double* cb = L.cin + b * L.cap;
-  double y[UW][NT][4];
-#pragma unroll
-  for (int u = 0; u < UW; ++u)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
-        y[u][nt][i] = (row < Call && row < R && c < t) ? cb[row + (int64_t)c * L.ldci] : 0.0;
-      }
-  wy_apply_panels<UW, NT>(y, L, P, b, r0, R, false, vbuf, red, Zp, pans, full);
-#pragma unroll
-  for (int u = 0; u < UW; ++u)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
-        if (row < R && c < ncol) L.Y[r0 + row + (int64_t)c * L.ldy] = c < t ? y[u][nt][i] : 0.0;
-      }
+__global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s) {
+  wy_body<UW, NT, true>(L, P, C, s, 0, 0);
+}
+
+// stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
+template <int UW, int NT>
+__global__ void __launch_bounds__(kWyLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
+  wy_body<UW, NT, false>(L, P, 0, t, Call, ncol);
 }
 
 }  // namespace pqr

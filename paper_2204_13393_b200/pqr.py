@@ -15,7 +15,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpqr.so")
+LIB_PATH = os.environ.get("PQR_LIB") or os.path.join(_HERE, "libpqr.so")  # PQR_LIB: A/B builds
 
 PQR_OK, PQR_EARG, PQR_ECAPACITY, PQR_EBREAKDOWN, PQR_EPLAN, PQR_ECUDA, PQR_ENCCL, PQR_ENOMEM = 0, -1, -2, -3, -4, -5, -6, -7
 PQR_CHOLQR2, PQR_TSQR = 0, 1

@@ -71,6 +71,35 @@ __global__ void k_dmma16816(double* out, int iters) {
   for (int j = 0; j < 4; ++j) s += d[j][0] + d[j][1] + d[j][2] + d[j][3];
   if (s == 1.2345) out[0] = s;
 }
+
+// DFMA and DMMA issued together: do the two fp64 pipes add up?  (mode 0: every warp
+// interleaves both; mode 1: even warps DMMA only, odd warps DFMA only)
+__global__ void k_mixed(double* out, int iters, int mode) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double d[8][2];
+  #pragma unroll
+  for (int j = 0; j < 8; ++j) d[j][0] = d[j][1] = 0;
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  const int warp = threadIdx.x >> 5;
+  const bool do_mma = mode == 0 || (warp & 1) == 0, do_fma = mode == 0 || (warp & 1) == 1;
+  for (int i = 0; i < iters; ++i) {
+    if (do_mma) {
+      #pragma unroll
+      for (int j = 0; j < 8; ++j) mma884(d[j][0], d[j][1], a, b);
+    }
+    if (do_fma) {
+      #pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+      }
+    }
+  }
+  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  #pragma unroll
+  for (int j = 0; j < 8; ++j) s += d[j][0] + d[j][1];
+  if (s == 1.2345) out[0] = s;
+}
 __global__ void k_clock(long long* out, int iters, double a) {
   long long t0 = clock64();
   double x = threadIdx.x;
@@ -145,6 +174,18 @@ int main() {
     }
     double flops = 2.0 * 16 * 8 * 16 * 4 * iters * (double)sms * 4 * (threads / 32);
     printf("{\"test\":\"dmma_m16n8k16\",\"threads\":%d,\"TFLOPs\":%.2f}\n", threads, flops / best / 1e9);
+  }
+  for (int mode : {0, 1}) {
+    int iters = 1 << 11, threads = 512;
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+      cudaEventRecord(e0); k_mixed<<<sms * 2, threads>>>(out, iters, mode); cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1); if (r && ms < best) best = ms;
+    }
+    // per iteration and warp: 8 DMMA (2*256*8 flop) and/or 64 DFMA per lane (2*64*32 flop)
+    double warps = (double)sms * 2 * (threads / 32);
+    double per_warp = mode == 0 ? 2.0 * 256 * 8 + 2.0 * 64 * 32 : 0.5 * (2.0 * 256 * 8 + 2.0 * 64 * 32);
+    printf("{\"test\":\"dmma+dfma\",\"mode\":%d,\"TFLOPs\":%.2f}\n", mode, per_warp * iters * warps / best / 1e9);
   }
   CK(cudaGetLastError());
   return 0;
