@@ -89,8 +89,8 @@ void wy_trace_dump(const char* kind, const WyLevel& L, cudaStream_t st) {
   cudaStreamSynchronize(st);
   cudaMemcpy(h, L.trace, sizeof(h), cudaMemcpyDeviceToHost);
   fprintf(stderr, "{\"wy_trace\": \"%s\", \"nblocks\": %d, \"rows\": %lld, \"w0\": [", kind, L.nblocks, (long long)L.q);
-  for (int i = 0; i < 10; ++i) fprintf(stderr, "%llu%s", h[i], i < 9 ? ", " : "], \"w15\": [");
-  for (int i = 0; i < 10; ++i) fprintf(stderr, "%llu%s", h[16 + i], i < 9 ? ", " : "]}\n");
+  for (int i = 0; i < 16; ++i) fprintf(stderr, "%llu%s", h[i], i < 15 ? ", " : "], \"w15\": [");
+  for (int i = 0; i < 16; ++i) fprintf(stderr, "%llu%s", h[16 + i], i < 15 ? ", " : "]}\n");
 }
 
 WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
@@ -272,7 +272,10 @@ int tsqr_alloc(Ctx* h) {
   const int wmax = ts->wmax;
   // node arity: even, node rows within the register/shared-memory budget
   const int rmax = wmax > 8 ? 512 : 1024;
-  ts->arity = std::max(2, std::min(8, (rmax / cap) & ~1));
+  // node rows arity*cap <= rmax, even (paired 16-byte rows): odd arity only with even cap
+  ts->arity = std::max(2, std::min(8, rmax / cap));
+  if ((cap & 1) && (ts->arity & 1)) ts->arity -= 1;
+  ts->arity = std::max(2, ts->arity);
   // leaf block rows: user's choice or ~1024 (512 when s_max > 8)
   int nb = h->cfg.block_rows > 0 ? h->cfg.block_rows : (wmax > 8 ? 512 : 1024);
   nb = std::max(nb, 2 * cap);

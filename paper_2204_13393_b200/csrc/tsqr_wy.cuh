@@ -38,7 +38,10 @@ namespace pqr {
 
 constexpr int kWyWarps = 16;
 constexpr int kWyThreads = 32 * kWyWarps;       // consumer threads
-constexpr int kWyLaunch = kWyThreads + 32;       // + one producer warp
+constexpr int kWyLaunch = kWyThreads + 128;      // + one producer warpgroup (one working lane)
+constexpr int kWyConsumerRegs = 112;  // setmaxnreg split of the launch allocation (640 x 96):
+                                      // 4 x 128 x 112 + 128 x 24 <= 640 x 96
+constexpr int kWyProducerRegs = 24;
 constexpr int kWyRowsPerUW = 16 * kWyWarps;  // block rows covered per unit-per-warp
 constexpr int kWyMaxW = 16;                  // widest panel
 constexpr int kWyHH = 2 * (kWyWarps * 16 + 16);  // Householder-round reduction buffers
@@ -118,8 +121,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 
   // ---- producer warp: streams ring item `it` into slot it % nbuf once the consumers have
   // released the slot's previous item (empty barrier, one arrival per consumer warp) ----
-  if (warp == kWyWarps) {
-    if (lane == 0) {
+  if (warp >= kWyWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWyProducerRegs));
+    if (warp == kWyWarps && lane == 0) {
       for (int it = 0; it < total; ++it) {
         const int jb = it / ipb;
         const int p = it - jb * ipb;
@@ -149,6 +153,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     }
     return;
   }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kWyConsumerRegs));
   // consumer warps only from here: named barrier 1 over the kWyThreads consumer threads
   auto cbar = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(kWyThreads) : "memory"); };
   // this warp is done with ring item `it` (all of its lanes' reads precede the arrival)
@@ -158,13 +163,20 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   };
   // fixed-order sum of the kWyWarps partials: G = kWyThreads / E threads per entry;
   // partials are entry-major with stride kWyWarps + 1 (conflict-free for writers and readers)
+  const int rz_G = kWyThreads / E;  // threads per entry (8 or 2)
+  const int rz_e = tid / rz_G, rz_part = tid - rz_e * rz_G;
+  const double* rz_src = red + rz_e * (kWyWarps + 1) + rz_part;
   auto reduce_Z = [&]() {
-    const int G = kWyThreads / E;
-    const int e = tid / G, part = tid - e * G;
-    double z = 0.0;
-    for (int ww = part; ww < kWyWarps; ww += G) z += red[e * (kWyWarps + 1) + ww];
-    for (int o = 1; o < G; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-    if (part == 0) Zs[e] = z;
+    double z = rz_src[0];
+    for (int ww = rz_G; ww < kWyWarps; ww += rz_G) z += rz_src[ww];
+    if (rz_G == 8) {
+      z += __shfl_xor_sync(0xffffffffu, z, 1);
+      z += __shfl_xor_sync(0xffffffffu, z, 2);
+      z += __shfl_xor_sync(0xffffffffu, z, 4);
+    } else {
+      z += __shfl_xor_sync(0xffffffffu, z, 1);
+    }
+    if (rz_part == 0) Zs[rz_e] = z;
   };
   // optional phase tracing (CTA 0, warps 0 and 15, lane 0): cycles per phase in smem
   __shared__ unsigned long long s_tr[2][16];
@@ -350,39 +362,61 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     } else {
     WY_TR(9);
     // ---------------- stage-1 tail: Householder QR of rows C..R-1 of the s new columns ----------------
+    // Warp classes per round (warp-uniform): rows all < r ("above": untouched, contributes 0),
+    // rows all > r ("interior": no row masks), or the warp holding pivot row r.
+    const int wr0 = 16 * UW * warp;
     for (int c = 0; c < s; ++c) {
       const int r = C + c;
       const int ntc = c >> 3, gc = c & 7;
       const int src = gc * 4 + q;
+      const bool above = wr0 + 16 * UW <= r;
+      const bool inter = wr0 > r;
+      const int rel = r - wr0 - 4 * q;  // row >= r  <=>  16u + i >= rel
       double xc[UW][4];
-#pragma unroll
-      for (int u = 0; u < UW; ++u)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          double v = x[u][0][i];
-          if (NT > 1 && ntc == 1) v = x[u][NT - 1][i];
-          xc[u][i] = __shfl_sync(0xffffffffu, v, src);
-        }
       double D[NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        double d = 0.0;
+      for (int nt = 0; nt < NT; ++nt) D[nt] = 0.0;
+      if (!above) {
 #pragma unroll
         for (int u = 0; u < UW; ++u)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (16 * (warp * UW + u) + 4 * q + i >= r) d = fma(xc[u][i], x[u][nt][i], d);
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);
-        D[nt] = d;
+          for (int i = 0; i < 4; ++i) {
+            double v = x[u][0][i];
+            if (NT > 1 && ntc == 1) v = x[u][NT - 1][i];
+            xc[u][i] = __shfl_sync(0xffffffffu, v, src);
+          }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double d0 = 0.0, d1 = 0.0;
+          if (inter) {
+#pragma unroll
+            for (int u = 0; u < UW; ++u)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                if (i & 1) d1 = fma(xc[u][i], x[u][nt][i], d1);
+                else d0 = fma(xc[u][i], x[u][nt][i], d0);
+              }
+          } else {
+#pragma unroll
+            for (int u = 0; u < UW; ++u)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (16 * u + i >= rel) d0 = fma(xc[u][i], x[u][nt][i], d0);
+          }
+          double d = d0 + d1;
+          d += __shfl_xor_sync(0xffffffffu, d, 1);
+          d += __shfl_xor_sync(0xffffffffu, d, 2);
+          D[nt] = d;
+        }
       }
+      WY_TR(10);
       double* hb = hred + hpar * (kWyWarps * 16 + 16);
       hpar ^= 1;
       if (q == 0) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) hb[warp * 16 + 8 * nt + g] = D[nt];
       }
-      {  // the owner of pivot row r broadcasts it (select chains: no dynamic register indexing)
+      if (!above && !inter) {  // the warp holding pivot row r broadcasts it (select chains)
         bool own_r = false;
         double xr[NT];
 #pragma unroll
@@ -391,7 +425,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         for (int u = 0; u < UW; ++u)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const bool hit = 16 * (warp * UW + u) + 4 * q + i == r;
+            const bool hit = 16 * u + i == rel;
             own_r |= hit;
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) xr[nt] = hit ? x[u][nt][i] : xr[nt];
@@ -401,41 +435,63 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int nt = 0; nt < NT; ++nt) hb[kWyWarps * 16 + 8 * nt + g] = xr[nt];
         }
       }
+      WY_TR(11);
       cbar();
-      double lam2 = 0.0, Dg[NT];
+      WY_TR(12);
+      if (above && warp != 0) continue;  // nothing to update (warp 0 records sigma*lambda)
+      // column sums of the 16 warp partials: lane (g, q) adds warps q, q+4, q+8, q+12, then
+      // a fixed xor tree over q; lambda^2 is column c's sum (from lane (gc, 0))
+      double Dg[NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) Dg[nt] = 0.0;
-#pragma unroll
-      for (int ww = 0; ww < kWyWarps; ++ww) {
-        lam2 += hb[ww * 16 + c];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) Dg[nt] += hb[ww * 16 + 8 * nt + g];
+      for (int nt = 0; nt < NT; ++nt) {
+        const double* hc = hb + 8 * nt + g;
+        double d = (hc[16 * q] + hc[16 * (q + 4)]) + (hc[16 * (q + 8)] + hc[16 * (q + 12)]);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);
+        Dg[nt] = d;
       }
+      const double lam2 = __shfl_sync(0xffffffffu, (NT > 1 && ntc == 1) ? Dg[NT - 1] : Dg[0], gc * 4);
       const double u0 = hb[kWyWarps * 16 + c];
       const double lam = sqrt(lam2);
       const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
       const double diag = sigma * lam;
       const double nv2 = 2.0 * lam * (lam + fabs(u0));
       const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
+      if (tid == 0) diagv[c] = diag;
+      if (above) continue;
       double f[NT];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int cc = 8 * nt + g;
         f[nt] = (cc > c && cc < s) ? 2.0 * inv * (Dg[nt] - diag * hb[kWyWarps * 16 + cc]) : 0.0;
       }
-      if (tid == 0) diagv[c] = diag;
+      WY_TR(13);
+      if (inter) {
 #pragma unroll
-      for (int u = 0; u < UW; ++u)
+        for (int u = 0; u < UW; ++u)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = 16 * (warp * UW + u) + 4 * q + i;
-          const double vv = row > r ? xc[u][i] * inv : (row == r ? (u0 - diag) * inv : 0.0);
+          for (int i = 0; i < 4; ++i) {
+            const double vv = xc[u][i] * inv;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const bool own = (nt == ntc) && (g == gc) && row >= r;
-            x[u][nt][i] = own ? vv : fma(-f[nt], vv, x[u][nt][i]);
+            for (int nt = 0; nt < NT; ++nt) {
+              const bool own = (nt == ntc) && (g == gc);
+              x[u][nt][i] = own ? vv : fma(-f[nt], vv, x[u][nt][i]);
+            }
           }
-        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UW; ++u)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = 16 * u + i;
+            const double vv = rr > rel ? xc[u][i] * inv : (rr == rel ? (u0 - diag) * inv : 0.0);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const bool own = (nt == ntc) && (g == gc) && rr >= rel;
+              x[u][nt][i] = own ? vv : fma(-f[nt], vv, x[u][nt][i]);
+            }
+          }
+      }
     }
 
     WY_TR(7);
