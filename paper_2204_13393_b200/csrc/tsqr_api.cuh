@@ -39,7 +39,11 @@ struct TsqrState {
   double* coef = nullptr;    // cap x 16 scratch for basis_apply
 };
 
-int uw_for(int64_t rows) { return (int)((rows + kWyRowsPerUW - 1) / kWyRowsPerUW); }
+// units of 16 rows per warp: even (the stage-1 tail gives every lane UW/2 whole rows)
+int uw_for(int64_t rows) {
+  const int uw = (int)((rows + kWyRowsPerUW - 1) / kWyRowsPerUW);
+  return uw + (uw & 1);
+}
 int rp_for(int UW) { return kWyRowsPerUW * UW + 10; }  // >= rows + 1, = 10 (mod 16)
 size_t wy_smem(int RP, int wmax, int cap, int nbuf) { return wy_smem_bytes(RP, wmax, cap, nbuf); }
 int nbuf_for(int RP, int wmax, int cap) {
@@ -66,11 +70,8 @@ cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int 
 
 #define PQR_WY_SWITCH(UW_, NT_, CALL)                                                        \
   switch ((UW_) * 10 + (NT_)) {                                                              \
-    case 11: e = CALL(1, 1); break; case 12: e = CALL(1, 2); break;                         \
     case 21: e = CALL(2, 1); break; case 22: e = CALL(2, 2); break;                         \
-    case 31: e = CALL(3, 1); break;                                                          \
     case 41: e = CALL(4, 1); break;                                                          \
-    case 51: e = CALL(5, 1); break;                                                          \
     case 61: e = CALL(6, 1); break;                                                          \
     default: return PQR_EPLAN;                                                               \
   }

@@ -78,7 +78,7 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
 // shared-memory bytes of a level kernel (host and device agree on this layout)
 inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
   const size_t E = (size_t)wmax * wmax;
-  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 256) * sizeof(double) +
+  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 512) * sizeof(double) +
          (size_t)((cap + 2) & ~1) * sizeof(int2) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
@@ -93,8 +93,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   double* Zs = red + (kWyWarps + 1) * E;   // E: reduced Z (ld wm)
   double* hred = Zs + E;                   // 2 x (kWyWarps*16 partials + 16 pivot-row values)
   double* diagv = hred + kWyHH;            // 16: sigma*lambda of the new columns
-  double* tsc = diagv + 16;                // 16 x 16: back-substitution scratch of the T columns
-  int2* pans = reinterpret_cast<int2*>(tsc + 256);
+  double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
+  int2* pans = reinterpret_cast<int2*>(tsc + 512);
   uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));
   uint64_t* empty = full + nbuf;
 
@@ -362,218 +362,165 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     } else {
     WY_TR(9);
     // ---------------- stage-1 tail: Householder QR of rows C..R-1 of the s new columns ----------------
-    // Warp classes per round (warp-uniform): rows all < r ("above": untouched, contributes 0),
-    // rows all > r ("interior": no row masks), or the warp holding pivot row r.
-    const int wr0 = 16 * UW * warp;
-    for (int c = 0; c < s; ++c) {
-      const int r = C + c;
-      const int ntc = c >> 3, gc = c & 7;
-      const int src = gc * 4 + q;
-      const bool above = wr0 + 16 * UW <= r;
-      const bool inter = wr0 > r;
-      const int rel = r - wr0 - 4 * q;  // row >= r  <=>  16u + i >= rel
-      double xc[UW][4];
-      double D[NT];
+    // Row layout: an 8-lane butterfly transpose inside every q-group gives lane (g, q) RPL = UW/2
+    // whole rows (all 8*NT columns), so each round's dot products are lane-local.  Round c:
+    //   D_c' = sum over rows >= r = C+c of x_c x_c' for every c' (one reduction: lane-local,
+    //   warp reduce-scatter, 16 warp partials), pivot row r broadcast; then every lane knows
+    //   v = (x_c - sigma*lambda e_r) / sqrt(2 lambda (lambda + |x_c[r]|)), sigma = -sgn(x_c[r]),
+    //   v . x_c' = (D_c' - sigma*lambda x_c'[r]) / sqrt(...) for c' > c (the update), and
+    //   v_c' . v_c by the same formula for c' < c (column c of V^T V, for T).
+    constexpr int RPL = UW / 2;   // rows per lane in the row layout
+    constexpr int S8 = 8 * NT;    // columns per row
+    double xr[RPL][S8];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) D[nt] = 0.0;
-      if (!above) {
+    for (int nt = 0; nt < NT; ++nt) {
+      double a[4 * UW];  // slot 4u + i of this lane's column 8nt + g; block p = slots p*RPL ..
 #pragma unroll
-        for (int u = 0; u < UW; ++u)
+      for (int u = 0; u < UW; ++u)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            double v = x[u][0][i];
-            if (NT > 1 && ntc == 1) v = x[u][NT - 1][i];
-            xc[u][i] = __shfl_sync(0xffffffffu, v, src);
+        for (int i = 0; i < 4; ++i) a[4 * u + i] = x[u][nt][i];
+      // element (lane g, block p) moves to (lane p, block g): swap one index bit per stage
+#pragma unroll
+      for (int mb = 4; mb >= 1; mb >>= 1) {
+        const bool up = (g & mb) != 0;
+#pragma unroll
+        for (int pb = 0; pb < 8; ++pb) {
+          if (pb & mb) continue;
+#pragma unroll
+          for (int e = 0; e < RPL; ++e) {
+            double& lo = a[pb * RPL + e];
+            double& hi = a[(pb | mb) * RPL + e];
+            const double recv = __shfl_xor_sync(0xffffffffu, up ? lo : hi, 4 * mb);
+            if (up) lo = recv; else hi = recv;
           }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          double d0 = 0.0, d1 = 0.0;
-          if (inter) {
-#pragma unroll
-            for (int u = 0; u < UW; ++u)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                if (i & 1) d1 = fma(xc[u][i], x[u][nt][i], d1);
-                else d0 = fma(xc[u][i], x[u][nt][i], d0);
-              }
-          } else {
-#pragma unroll
-            for (int u = 0; u < UW; ++u)
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (16 * u + i >= rel) d0 = fma(xc[u][i], x[u][nt][i], d0);
-          }
-          double d = d0 + d1;
-          d += __shfl_xor_sync(0xffffffffu, d, 1);
-          d += __shfl_xor_sync(0xffffffffu, d, 2);
-          D[nt] = d;
         }
       }
-      WY_TR(10);
+#pragma unroll
+      for (int pb = 0; pb < 8; ++pb)
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) xr[e][8 * nt + pb] = a[pb * RPL + e];
+    }
+    int rowk[RPL];  // block-local rows of this lane
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+      const int sg = g * RPL + e;
+      rowk[e] = 16 * (warp * UW + (sg >> 2)) + 4 * q + (sg & 3);
+    }
+    double* Gs = tsc;  // strict upper part of V^T V (ld 16), column c written in round c by tid 0
+    WY_TR(10);
+#pragma unroll
+    for (int c = 0; c < S8; ++c) {
+      if (c >= s) break;
+      const int r = C + c;
+      double D[S8];
+#pragma unroll
+      for (int cc = 0; cc < S8; ++cc) D[cc] = 0.0;
+#pragma unroll
+      for (int e = 0; e < RPL; ++e)
+        if (rowk[e] >= r) {
+#pragma unroll
+          for (int cc = 0; cc < S8; ++cc) D[cc] = fma(xr[e][c], xr[e][cc], D[cc]);
+        }
+      // warp reduce-scatter of the S8 values (fixed xor tree): lane ends with value vi
+#pragma unroll
+      for (int mb = 16, w = S8; w > 1; mb >>= 1, w >>= 1) {
+        const bool up = (lane & mb) != 0;
+#pragma unroll
+        for (int j = 0; j < w / 2; ++j) {
+          const double send = up ? D[j] : D[j + w / 2];
+          const double keep = up ? D[j + w / 2] : D[j];
+          D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
+        }
+      }
+      constexpr int LG = S8 == 8 ? 4 : 2;  // lanes sharing a value after the scatter
+      D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
+      if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
+      const int vi = (lane / LG) & (S8 - 1);
       double* hb = hred + hpar * (kWyWarps * 16 + 16);
       hpar ^= 1;
-      if (q == 0) {
+      if ((lane & (LG - 1)) == 0) hb[warp * 16 + vi] = D[0];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) hb[warp * 16 + 8 * nt + g] = D[nt];
-      }
-      if (!above && !inter) {  // the warp holding pivot row r broadcasts it (select chains)
-        bool own_r = false;
-        double xr[NT];
+      for (int e = 0; e < RPL; ++e)
+        if (rowk[e] == r) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) xr[nt] = 0.0;
-#pragma unroll
-        for (int u = 0; u < UW; ++u)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const bool hit = 16 * u + i == rel;
-            own_r |= hit;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) xr[nt] = hit ? x[u][nt][i] : xr[nt];
-          }
-        if (own_r) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) hb[kWyWarps * 16 + 8 * nt + g] = xr[nt];
+          for (int cc = 0; cc < S8; ++cc) hb[kWyWarps * 16 + cc] = xr[e][cc];
         }
-      }
       WY_TR(11);
       cbar();
       WY_TR(12);
-      if (above && warp != 0) continue;  // nothing to update (warp 0 records sigma*lambda)
-      // column sums of the 16 warp partials: lane (g, q) adds warps q, q+4, q+8, q+12, then
-      // a fixed xor tree over q; lambda^2 is column c's sum (from lane (gc, 0))
-      double Dg[NT];
+      // sums over the 16 warps (lane: value lane % S8, a quarter/half of the warps), broadcast
+      double tot;
+      {
+        constexpr int NP = 32 / S8, WPP = kWyWarps / NP;  // lane groups, warps per group
+        const int v = lane & (S8 - 1), part = lane / S8;
+        const double* hv = hb + part * WPP * 16 + v;
+        tot = 0.0;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const double* hc = hb + 8 * nt + g;
-        double d = (hc[16 * q] + hc[16 * (q + 4)]) + (hc[16 * (q + 8)] + hc[16 * (q + 12)]);
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);
-        Dg[nt] = d;
+        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * 16];
+#pragma unroll
+        for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
       }
-      const double lam2 = __shfl_sync(0xffffffffu, (NT > 1 && ntc == 1) ? Dg[NT - 1] : Dg[0], gc * 4);
+      double Dt[S8];
+#pragma unroll
+      for (int cc = 0; cc < S8; ++cc) Dt[cc] = __shfl_sync(0xffffffffu, tot, cc);
       const double u0 = hb[kWyWarps * 16 + c];
-      const double lam = sqrt(lam2);
+      const double lam = sqrt(Dt[c]);
       const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
       const double diag = sigma * lam;
       const double nv2 = 2.0 * lam * (lam + fabs(u0));
       const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
-      if (tid == 0) diagv[c] = diag;
-      if (above) continue;
-      double f[NT];
+      double f[S8];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int cc = 8 * nt + g;
-        f[nt] = (cc > c && cc < s) ? 2.0 * inv * (Dg[nt] - diag * hb[kWyWarps * 16 + cc]) : 0.0;
+      for (int cc = 0; cc < S8; ++cc) f[cc] = cc == c ? 0.0 : 2.0 * inv * (Dt[cc] - diag * hb[kWyWarps * 16 + cc]);
+      if (tid == 0) {
+        diagv[c] = diag;
+#pragma unroll
+        for (int cc = 0; cc < c; ++cc) Gs[cc + 16 * c] = 0.5 * f[cc];  // v_cc . v_c
       }
       WY_TR(13);
-      if (inter) {
 #pragma unroll
-        for (int u = 0; u < UW; ++u)
+      for (int e = 0; e < RPL; ++e)
+        if (rowk[e] >= r) {
+          const double vv = (rowk[e] == r ? u0 - diag : xr[e][c]) * inv;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const double vv = xc[u][i] * inv;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const bool own = (nt == ntc) && (g == gc);
-              x[u][nt][i] = own ? vv : fma(-f[nt], vv, x[u][nt][i]);
-            }
-          }
-      } else {
-#pragma unroll
-        for (int u = 0; u < UW; ++u)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rr = 16 * u + i;
-            const double vv = rr > rel ? xc[u][i] * inv : (rr == rel ? (u0 - diag) * inv : 0.0);
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const bool own = (nt == ntc) && (g == gc) && rr >= rel;
-              x[u][nt][i] = own ? vv : fma(-f[nt], vv, x[u][nt][i]);
-            }
-          }
-      }
+          for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-f[cc], vv, xr[e][cc]);
+          xr[e][c] = vv;
+        }
     }
-
     WY_TR(7);
-    // ---------------- T of the new panel: T^{-1} = I/2 + striu(V^T V) ----------------
-    {
-      double ac[NT][NT][2];
-#pragma unroll
-      for (int mt = 0; mt < NT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) ac[mt][nt][0] = ac[mt][nt][1] = 0.0;
-#pragma unroll
-      for (int u = 0; u < UW; ++u)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = 16 * (warp * UW + u) + 4 * q + i;
-          double vr[NT];
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const int cc = 8 * nt + g;
-            vr[nt] = (cc < s && row >= C + cc) ? x[u][nt][i] : 0.0;
-          }
-#pragma unroll
-          for (int mt = 0; mt < NT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma884(ac[mt][nt][0], ac[mt][nt][1], vr[mt], vr[nt]);
-        }
-#pragma unroll
-      for (int mt = 0; mt < NT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) red[((8 * mt + g) + wm * (8 * nt + 2 * q + v)) * (kWyWarps + 1) + warp] = ac[mt][nt][v];
-      cbar();
-      reduce_Z();
-      cbar();
-      double* Tn = L.T + b * L.tstride + 16 * C;
-      if (tid < s) {  // column c of T by back substitution
-        const int c = tid;
-        double* col = tsc + 16 * c;  // own area: with no panels the next block's rounds follow
-                                     // without a barrier and reuse hred
-        for (int i = 0; i < kWyMaxW; ++i) col[i] = 0.0;
-        col[c] = 2.0;  // 1 / (1/2)
-        for (int i = c - 1; i >= 0; --i) {
-          double a = 0.0;
-          for (int l = i + 1; l <= c; ++l) a += Zs[i + wm * l] * col[l];
-          col[i] = -a * 2.0;
-        }
-        for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
+    // ---------------- T of the new panel: T^{-1} = I/2 + striu(V^T V) (warp 0) ----------------
+    __syncwarp();
+    if (tid < s) {
+      const int c = tid;
+      double* col = tsc + 256 + 16 * c;
+      for (int i = 0; i < kWyMaxW; ++i) col[i] = 0.0;
+      col[c] = 2.0;  // 1 / (1/2)
+      for (int i = c - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int l = i + 1; l <= c; ++l) acc += Gs[i + 16 * l] * col[l];
+        col[i] = -acc * 2.0;
       }
+      double* Tn = L.T + b * L.tstride + 16 * C;
+      for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
     }
-
+    __syncwarp();
     WY_TR(8);
     // ---------------- outputs: [P_b; N_b] to the parent slot, the new reflectors ----------------
     {
       double* outb = L.out + b * L.cap;
       const int rmax = R < L.cap ? R : L.cap;
 #pragma unroll
-      for (int u = 0; u < UW; ++u)
+      for (int c = 0; c < S8; ++c) {
+        if (c >= s) break;
+        const int piv = C + c;
+        const double dg = diagv[c];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int c = 8 * nt + g;
-          if (c >= s) continue;
-          const int piv = C + c;
-          const double dg = diagv[c];
-          const int row0 = 16 * (warp * UW + u) + 4 * q;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int row = row0 + i;
-            if (row < rmax) outb[row + (int64_t)c * L.ldo] = row < piv ? x[u][nt][i] : (row == piv ? dg : 0.0);
-          }
-          double* vp = L.V + r0 + row0 + (int64_t)(C + c) * L.ldv;
-#pragma unroll
-          for (int i = 0; i < 4; i += 2) {
-            const int row = row0 + i;
-            const double v0 = row >= piv ? x[u][nt][i] : 0.0, v1 = row + 1 >= piv ? x[u][nt][i + 1] : 0.0;
-            if (row + 1 < R) {
-              st2(vp + i, v0, v1);
-            } else if (row < R) {
-              vp[i] = v0;
-            }
-          }
+        for (int e = 0; e < RPL; ++e) {
+          const int row = rowk[e];
+          if (row < rmax) outb[row + (int64_t)c * L.ldo] = row < piv ? xr[e][c] : (row == piv ? dg : 0.0);
+          if (row < R) L.V[r0 + row + (int64_t)(C + c) * L.ldv] = row >= piv ? xr[e][c] : 0.0;
         }
+      }
     }
     }  // stage-1 tail
   }
