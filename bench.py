@@ -374,7 +374,7 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
-            _, cpu, _ = oracle_sample(w, target_s=15.0)
+            _, cpu, _ = oracle_sample(w, target_s=25.0)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "error": str(e)}
 
