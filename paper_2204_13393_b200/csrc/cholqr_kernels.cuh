@@ -137,19 +137,7 @@ __global__ void __launch_bounds__(256) k_gram(GramArgs a) {
   __threadfence();
   const int ms = m * a.s;
   const int nb = gridDim.x;
-  for (int e = threadIdx.x; e < ms; e += blockDim.x) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {
-      s0 += __ldcg(a.partials + (size_t)(b + 0) * ms + e);
-      s1 += __ldcg(a.partials + (size_t)(b + 1) * ms + e);
-      s2 += __ldcg(a.partials + (size_t)(b + 2) * ms + e);
-      s3 += __ldcg(a.partials + (size_t)(b + 3) * ms + e);
-    }
-    for (; b < nb; ++b) s0 += __ldcg(a.partials + (size_t)b * ms + e);
-    const int j = e % m, c = e / m;
-    a.W[j + (int64_t)c * a.ldw] = (s0 + s1) + (s2 + s3);
-  }
+  grid_sum_partials(a.partials, nb, ms, m, a.W, a.ldw);
   if (threadIdx.x == 0) *a.ticket = 0u;
 }
 

@@ -140,3 +140,26 @@ PQR_DEV void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 }  // namespace pqr
+
+namespace pqr {
+// Grid reduction by the last CTA: W(j, c) = sum over the nb per-CTA partials (ms = m*s entries,
+// column-major m x s each, at partials + b*ms).  Partial b goes to accumulator b % 4, the four
+// are combined as (a0 + a1) + (a2 + a3): a fixed order, so results are bitwise reproducible.
+// 16 independent L2 loads per thread are in flight per step (the reduction is latency-bound).
+PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, double* W, int ldw) {
+  for (int e = threadIdx.x; e < ms; e += blockDim.x) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int b = 0;
+    for (; b + 16 <= nb; b += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldcg(partials + (size_t)(b + u) * ms + e);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u & 3] += v[u];
+    }
+    for (; b < nb; ++b) acc[b & 3] += __ldcg(partials + (size_t)b * ms + e);
+    const int jj = e % m, c = e / m;
+    W[jj + (int64_t)c * ldw] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  }
+}
+}  // namespace pqr

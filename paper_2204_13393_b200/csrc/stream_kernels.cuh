@@ -204,19 +204,7 @@ __global__ void __launch_bounds__(kCpaThreads, 2) k_gram_cpa(GramCpaArgs a) {
   __threadfence();
   const int ms = m * s;
   const int nb = gridDim.x;
-  for (int e = tid; e < ms; e += kCpaThreads) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {
-      s0 += __ldcg(a.partials + (size_t)(b + 0) * ms + e);
-      s1 += __ldcg(a.partials + (size_t)(b + 1) * ms + e);
-      s2 += __ldcg(a.partials + (size_t)(b + 2) * ms + e);
-      s3 += __ldcg(a.partials + (size_t)(b + 3) * ms + e);
-    }
-    for (; b < nb; ++b) s0 += __ldcg(a.partials + (size_t)b * ms + e);
-    const int jj = e % m, c = e / m;
-    a.W[jj + (int64_t)c * a.ldw] = (s0 + s1) + (s2 + s3);
-  }
+  grid_sum_partials(a.partials, nb, ms, m, a.W, a.ldw);
   if (tid == 0) *a.ticket = 0u;
 }
 
@@ -447,19 +435,7 @@ __global__ void __launch_bounds__(kCpaThreads, NT == 1 ? 2 : 1) k_update_gram_cp
   __threadfence();
   const int ms = m * s;
   const int nb = gridDim.x;
-  for (int e = tid; e < ms; e += kCpaThreads) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {
-      s0 += __ldcg(a.partials + (size_t)(b + 0) * ms + e);
-      s1 += __ldcg(a.partials + (size_t)(b + 1) * ms + e);
-      s2 += __ldcg(a.partials + (size_t)(b + 2) * ms + e);
-      s3 += __ldcg(a.partials + (size_t)(b + 3) * ms + e);
-    }
-    for (; b < nb; ++b) s0 += __ldcg(a.partials + (size_t)b * ms + e);
-    const int jj = e % m, c = e / m;
-    a.W[jj + (int64_t)c * a.ldw] = (s0 + s1) + (s2 + s3);
-  }
+  grid_sum_partials(a.partials, nb, ms, m, a.W, a.ldw);
   if (tid == 0) *a.ticket = 0u;
 }
 
