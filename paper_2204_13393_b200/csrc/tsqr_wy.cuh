@@ -44,7 +44,8 @@ constexpr int kWyConsumerRegs = 112;  // setmaxnreg split of the launch allocati
 constexpr int kWyProducerRegs = 24;
 constexpr int kWyRowsPerUW = 16 * kWyWarps;  // block rows covered per unit-per-warp
 constexpr int kWyMaxW = 16;                  // widest panel
-constexpr int kWyHH = 2 * (kWyWarps * 16 + 16);  // Householder-round reduction buffers
+constexpr int kWyHS = 17;                          // Householder-round partials: row stride (padded)
+constexpr int kWyHH = 2 * (kWyWarps * kWyHS + 16);  // Householder-round reduction buffers
 
 struct WyLevel {
   int64_t q, rem2;      // block b: q + 2*(b < rem2) rows starting at b*q + 2*min(b, rem2) (even);
@@ -436,14 +437,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
       if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
       const int vi = (lane / LG) & (S8 - 1);
-      double* hb = hred + hpar * (kWyWarps * 16 + 16);
+      double* hb = hred + hpar * (kWyWarps * kWyHS + 16);
       hpar ^= 1;
-      if ((lane & (LG - 1)) == 0) hb[warp * 16 + vi] = D[0];
+      if ((lane & (LG - 1)) == 0) hb[warp * kWyHS + vi] = D[0];
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
         if (rowk[e] == r) {
 #pragma unroll
-          for (int cc = 0; cc < S8; ++cc) hb[kWyWarps * 16 + cc] = xr[e][cc];
+          for (int cc = 0; cc < S8; ++cc) hb[kWyWarps * kWyHS + cc] = xr[e][cc];
         }
       WY_TR(11);
       cbar();
@@ -453,17 +454,19 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       {
         constexpr int NP = 32 / S8, WPP = kWyWarps / NP;  // lane groups, warps per group
         const int v = lane & (S8 - 1), part = lane / S8;
-        const double* hv = hb + part * WPP * 16 + v;
+        const double* hv = hb + part * WPP * kWyHS + v;
         tot = 0.0;
 #pragma unroll
-        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * 16];
+        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
 #pragma unroll
         for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
       }
+      WY_TR(14);
       double Dt[S8];
 #pragma unroll
       for (int cc = 0; cc < S8; ++cc) Dt[cc] = __shfl_sync(0xffffffffu, tot, cc);
-      const double u0 = hb[kWyWarps * 16 + c];
+      const double u0 = hb[kWyWarps * kWyHS + c];
+      WY_TR(15);
       const double lam = sqrt(Dt[c]);
       const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
       const double diag = sigma * lam;
@@ -471,7 +474,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
       double f[S8];
 #pragma unroll
-      for (int cc = 0; cc < S8; ++cc) f[cc] = cc == c ? 0.0 : 2.0 * inv * (Dt[cc] - diag * hb[kWyWarps * 16 + cc]);
+      for (int cc = 0; cc < S8; ++cc) f[cc] = cc == c ? 0.0 : 2.0 * inv * (Dt[cc] - diag * hb[kWyWarps * kWyHS + cc]);
       if (tid == 0) {
         diagv[c] = diag;
 #pragma unroll
