@@ -157,7 +157,11 @@ PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, do
 #pragma unroll
       for (int u = 0; u < 16; ++u) acc[u & 3] += v[u];
     }
-    for (; b < nb; ++b) acc[b & 3] += __ldcg(partials + (size_t)b * ms + e);
+    for (; b < nb; b += 4) {  // b is a multiple of 4 here: partial b + u goes to acc[u]
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b + u < nb) acc[u] += __ldcg(partials + (size_t)(b + u) * ms + e);
+    }
     const int jj = e % m, c = e / m;
     W[jj + (int64_t)c * ldw] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
