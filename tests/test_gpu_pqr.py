@@ -52,7 +52,8 @@ def check_vs_oracle(out, ref, tol=1e-10):
 
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("n,k,s", [(10_000, 32, 4), (4097, 13, 3), (20_000, 0, 8), (65_536, 128, 8),
-                                   (30_001, 96, 16), (12, 3, 2), (300_007, 64, 8)])
+                                   (30_001, 96, 16), (12, 3, 2), (300_007, 64, 8),
+                                   (20_011, 144, 16), (50_000, 152, 8)])  # last two: k + s = kMMax
 def test_vs_oracle_random(P, orc, variant, n, k, s):
     Q = inputs.orthonormal(7 + n, n, k)
     X = inputs.gaussian(8 + n, n, s)
