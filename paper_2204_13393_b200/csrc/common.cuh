@@ -15,6 +15,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #define PQR_DEV __device__ __forceinline__
 
 namespace pqr {
@@ -165,5 +168,22 @@ PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, do
     const int jj = e % m, c = e / m;
     W[jj + (int64_t)c * ldw] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
+}
+}  // namespace pqr
+
+namespace pqr {
+// Host: raise a kernel's dynamic shared-memory limit to `bytes` once (cached per kernel, so
+// repeated launches do not pay a cudaFuncSetAttribute call each).
+template <typename K>
+inline cudaError_t ensure_smem(K kern, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  const void* key = reinterpret_cast<const void*>(kern);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
 }
 }  // namespace pqr

@@ -189,11 +189,11 @@ template <int MTW, int NT>
 cudaError_t launch_gram_t(const GramPlan& p, const GramArgs& a, bool vec, cudaStream_t st) {
   if (vec) {
     auto f = k_gram<MTW, NT, true>;
-    if (p.smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (p.smem > 48 * 1024) ensure_smem(f, p.smem);
     f<<<p.grid, kThreads, p.smem, st>>>(a);
   } else {
     auto f = k_gram<MTW, NT, false>;
-    if (p.smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (p.smem > 48 * 1024) ensure_smem(f, p.smem);
     f<<<p.grid, kThreads, p.smem, st>>>(a);
   }
   return cudaGetLastError();
@@ -216,7 +216,7 @@ constexpr int kSmemBudget = 225 * 1024;
 template <int MTH, int NT, int RB>
 cudaError_t launch_gram_cpa_t(int grid, size_t smem, const GramCpaArgs& a, cudaStream_t st) {
   auto f = k_gram_cpa<MTH, NT, RB>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(f, smem);
   f<<<grid, kCpaThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -308,7 +308,7 @@ int run_update(int64_t n, int k, const double* Q, int64_t ldq, int sx, const dou
     const size_t sm2 = smM + NS * stg + 2 * NS * sizeof(uint64_t);
     const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * ctas, (n + kUpdRB - 1) / kUpdRB));
     auto go = [&](auto kern) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      ensure_smem(kern, sm2);
       kern<<<g2, kCpaThreads, sm2, st>>>(b);
     };
     if (NT == 1) {
@@ -348,7 +348,7 @@ int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches) {
 template <int MTH, int NT>
 cudaError_t launch_update_gram_t(int grid, size_t smem, const UpdGramArgs& a, cudaStream_t st) {
   auto f = k_update_gram_cpa<MTH, NT>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(f, smem);
   f<<<grid, kCpaThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -497,10 +497,11 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
     CUDA_TRY(cudaMemcpyAsync(h->Nf, h->N1, sizeof(double) * kSMax * kSMax, cudaMemcpyDeviceToDevice, h->stream));
     CUDA_TRY(cudaMemcpyAsync(h->ints + 2, d_t1, sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
   }
+  // t (ints[2]) and the deflation count (ints[3]) reach the host with the caller's single
+  // synchronisation in pqr_project_normalize
   CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(cudaStreamSynchronize(h->stream));
-  *t_host = h->h_ints[2];
-  if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;
+  (void)t_host;
+  (void)flags;
   return PQR_OK;
 }
 
@@ -676,7 +677,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
     rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
   }
   if (rc != PQR_OK) return rc;
-  // outputs
+  // outputs (enqueued before the one synchronisation of the call)
   if (U && Ud != U) {
     CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, ldud * sizeof(double), n * sizeof(double), s,
                                cudaMemcpyDefault, h->stream));
@@ -689,6 +690,9 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
                                (size_t)s * sizeof(double), s, cudaMemcpyDefault, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   prof_collect(h);
+  tt = h->h_ints[2];
+  if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;  // basis unchanged
+  if (append && h->cfg.variant == PQR_TSQR) TRY(tsqr_commit(h, s, tt));
   *t = tt;
   if (append) h->k += tt;
   h->st.calls += 1;

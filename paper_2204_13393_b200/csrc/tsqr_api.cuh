@@ -55,7 +55,7 @@ int nbuf_for(int RP, int wmax, int cap) {
 template <int UW, int NT>
 cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int grid, size_t smem, cudaStream_t st) {
   auto f = k_wy_up<UW, NT>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(f, smem);
   f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s);
   return cudaGetLastError();
 }
@@ -63,7 +63,7 @@ template <int UW, int NT>
 cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
                       cudaStream_t st) {
   auto f = k_wy_down<UW, NT>;
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(f, smem);
   f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
   return cudaGetLastError();
 }
@@ -383,12 +383,12 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
   TRY(tsqr_stage_panel(h, s));
   // U~ columns >= t are zero, so the down sweep writes zeros there.
   TRY(tsqr_down_sweep(h, np + 1, ts->C + s, ts->Ut, s, s, Ud, ldud));
+  // t reaches the host with the caller's single synchronisation; the caller commits the
+  // panel (tsqr_commit) once t is known and the call has not failed
   CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_TRY(cudaStreamSynchronize(h->stream));
-  const int t = h->h_ints[2];
-  *t_host = t;
-  if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;
-  if (append) TRY(tsqr_commit(h, s, t));
+  (void)t_host;
+  (void)flags;
+  (void)append;
   return PQR_OK;
 }
 
