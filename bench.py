@@ -250,12 +250,16 @@ def main():
 
     from paper_2204_13393_b200 import dist as pdist
 
-    nccl_id = pdist.nccl_id_for_library(world)
-
+    # the weak workload is one global problem row-sharded over the ranks (the library's NCCL
+    # exchange joins them); the other workloads run as independent replicas per rank
+    sharded = args.workload == "weak" and world > 1
     variants = ["cholqr2", "tsqr"] if args.variant == "both" else [args.variant]
     handles = {}
     for v in variants:
-        handles[v] = pqr.PQR(n, k, s, Q, variant=v, stream=stream, rank=rank, nranks=world, nccl_id=nccl_id)
+        # one ncclUniqueId per communicator (each handle owns one)
+        nccl_id = pdist.nccl_id_for_library(world) if sharded else None
+        handles[v] = pqr.PQR(n, k, s, Q, variant=v, stream=stream, rank=rank if sharded else 0,
+                             nranks=world if sharded else 1, nccl_id=nccl_id)
     del Q
     torch.cuda.empty_cache()
 
@@ -386,7 +390,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "baseline_config": w["cfg_index"], "n_local": n, "k": k, "s": s,
-                       "global_rows": n * world, "variants": variants, "parallelism": f"dp{world}",
+                       "global_rows": n * world if sharded or world == 1 else n, "variants": variants,
+                       "parallelism": f"dp{world}" if sharded or world == 1 else f"replicas{world}",
                        "l2": "inputs exceed L2 (no flush needed)" if mandatory_bytes(n, k, s) > 2 * 126e6
                        else "inputs fit in L2 (latency-bound config)",
                        "t": t_vals},

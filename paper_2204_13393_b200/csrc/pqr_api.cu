@@ -410,7 +410,7 @@ int gram_and_exchange(Ctx* h, int k, int s, const double* Q, const double* X, in
 
 // (nranks > 1) allgather this rank's Gram so every rank sums all ranks' in rank order
 int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts) {
-  if (h->cfg.nranks > 1) {
+  if (h->comm) {
     PROF(h, PQR_K_NCCL);
     NCCL_TRY(ncclAllGather(h->Wloc, h->Wall, (size_t)m * s, ncclDouble, h->comm, h->stream));
     h->st.collectives += 1;
@@ -576,9 +576,16 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   if (cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
   if (cudaMemsetAsync(h->ints, 0, 64 * sizeof(int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
 
-  if (cfg->nranks > 1) {
+  // PQR_FORCE_NCCL=1 (test aid): a single-rank handle still builds its communicator and runs
+  // every cross-GPU step (allgathers, the replicated cross-GPU tree node) with one rank.
+  static const bool force_nccl = getenv("PQR_FORCE_NCCL") && atoi(getenv("PQR_FORCE_NCCL")) != 0;
+  if (cfg->nranks > 1 || force_nccl) {
     ncclUniqueId id;
-    memcpy(&id, cfg->nccl_id, sizeof(id));
+    if (cfg->nccl_id) {
+      memcpy(&id, cfg->nccl_id, sizeof(id));
+    } else if (ncclGetUniqueId(&id) != ncclSuccess) {
+      return fail(PQR_ENCCL);
+    }
     ncclResult_t r = ncclCommInitRank(&h->comm, cfg->nranks, id, cfg->rank);
     if (r != ncclSuccess) {
       fprintf(stderr, "[pqr] ncclCommInitRank: %s\n", ncclGetErrorString(r));

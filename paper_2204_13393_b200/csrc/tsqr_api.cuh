@@ -167,7 +167,7 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s) {
                     root ? ts->cap : ts->lv[l + 1].rows, np, C, s));
     }
   }
-  if (h->cfg.nranks > 1) {
+  if (h->comm) {
     const int P = h->cfg.nranks;
     {
       PROF(h, PQR_K_NCCL);
@@ -193,7 +193,7 @@ int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol
   int64_t root_ld = ts->cap;
   {
     PROF(h, PQR_K_TSQR_TREE);
-    if (h->cfg.nranks > 1) {
+    if (h->comm) {
       TRY(run_wy_down(h, ts->xl, cin, ts->cap, ts->xl.dn, ts->xl.rows, np, Call, t, ncol));
       root_cin = ts->xl.dn + (int64_t)h->cfg.rank * ts->cap;
       root_ld = ts->xl.rows;
@@ -317,7 +317,7 @@ int tsqr_alloc(Ctx* h) {
   CUDA_TRY(cudaMemsetAsync(ts->Rt, 0, sizeof(double) * cap * cap, h->stream));
   if ((rc = dalloc(&ts->coef, (size_t)cap * 16))) return rc;
   if ((rc = dalloc(&ts->d_pan, (size_t)cap + 1))) return rc;
-  if (h->cfg.nranks > 1) {
+  if (h->comm) {
     TsqrLv& x = ts->xl;
     x.nblocks = 1;
     x.q = (int64_t)h->cfg.nranks * cap;
