@@ -42,6 +42,25 @@ WORKLOADS = {
 METRIC = "PQR effective HBM GB/s (fraction of roofline) at 1/2/4/8 B200, fp64"
 
 
+# The JSON line is the only thing this script writes to stdout: C-level output of the libraries
+# (e.g. NCCL's version banner from the communicator the library builds) is redirected to
+# stderr at start-up, and the line goes to a saved duplicate of the original stdout.
+_JSON_FD = None
+
+
+def _claim_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    out = (json.dumps(line) + "\n").encode()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, out)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -186,7 +205,7 @@ def run_reference(args, rank, world):
                        "sample_rows": rows, "parallelism": f"dp{world}"},
             "cpu_baseline": info,
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -404,7 +423,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -483,11 +502,12 @@ def run_arnoldi(args, rank, world, local_rank, device):
                 "cpu_baseline": None, "e2e": None,
                 "gpu_launches": sum(d["launches"] for d in kinds.values()) // max(1, args.steps),
                 "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
 if __name__ == "__main__":
+    _claim_stdout()
     sys.exit(main())
