@@ -699,7 +699,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   prof_collect(h);
   tt = h->h_ints[2];
   if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;  // basis unchanged
-  if (append && h->cfg.variant == PQR_TSQR) TRY(tsqr_commit(h, s, tt));
+  if (append && h->cfg.variant == PQR_TSQR) TRY(tsqr_commit(h, s, tt, h->ts->merge, h->ts->mtoff));
   *t = tt;
   if (append) h->k += tt;
   h->st.calls += 1;

@@ -29,8 +29,10 @@ struct TsqrState {
   int nb = 0, cap = 0, C = 0, nlev = 0, arity = 8, wmax = 8;
   std::vector<TsqrLv> lv;    // [0] leaves, [1..nlev] nodes
   TsqrLv xl;                 // cross-GPU node
-  std::vector<int2> panels;  // committed panels (start, width)
-  int2* d_pan = nullptr;     // device copy (+ one uncommitted slot)
+  std::vector<int4> panels;  // committed panels (start, width, T offset, merged)
+  int4* d_pan = nullptr;     // device copy (+ one uncommitted slot)
+  int4* d_panm = nullptr;    // down-sweep list of a merging call
+  int merge = 0, mtoff = 0;  // the last call merged its panel into the previous one
   double* in_top = nullptr;  // cap x wmax: GPU root stage-1 output (ld cap)
   double* xraw = nullptr;    // nranks * cap * wmax allgather receive
   double* Btop = nullptr;    // cap x wmax top coefficients of X (ld cap)
@@ -53,10 +55,11 @@ int nbuf_for(int RP, int wmax, int cap) {
 }
 
 template <int UW, int NT>
-cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int grid, size_t smem, cudaStream_t st) {
+cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
+                    cudaStream_t st) {
   auto f = k_wy_up<UW, NT>;
   ensure_smem(f, smem);
-  f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s);
+  f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
   return cudaGetLastError();
 }
 template <int UW, int NT>
@@ -104,7 +107,7 @@ WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
 }
 
 int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* out, int64_t ldo, int np, int C,
-              int s) {
+              int s, int merge = 0, int mtoff = 0) {
   TsqrState* ts = h->ts;
   WyLevel L = to_wy(ts, lv);
   L.X = X; L.ldx = ldx; L.out = out; L.ldo = ldo;
@@ -113,7 +116,7 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
   const int grid = std::min(lv.nblocks, h->sms);
   cudaError_t e;
-#define UPC(U, N) wy_up_t<U, N>(L, P, C, s, grid, smem, h->stream)
+#define UPC(U, N) wy_up_t<U, N>(L, P, C, s, merge, mtoff, grid, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, UPC)
 #undef UPC
   wy_trace_dump("up", L, h->stream);
@@ -126,12 +129,12 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
 }
 
 int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, double* Y, int64_t ldy, int np,
-                int Call, int t, int ncol) {
+                int Call, int t, int ncol, const int4* pan) {
   TsqrState* ts = h->ts;
   WyLevel L = to_wy(ts, lv);
   L.cin = cin; L.ldci = ldci; L.Y = Y; L.ldy = ldy;
   L.yvec = ((ldy & 1) == 0 && aligned16(Y)) ? 1 : 0;
-  WyPanels P{ts->d_pan, np};
+  WyPanels P{pan, np};
   const int NT = ncol > 8 ? 2 : 1;
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
   const int grid = std::min(lv.nblocks, h->sms);
@@ -150,21 +153,21 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
 
 // Stage 1 over all levels: X (n_local x s) -> Btop ((C+s) x s, ld cap).  Creates s new
 // reflectors (one new panel) at every level.
-int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s) {
+int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, int mtoff = 0) {
   TsqrState* ts = h->ts;
   const int C = ts->C;
   const int np = (int)ts->panels.size();
   {
     PROF(h, PQR_K_TSQR_LOCAL);
     TRY(run_wy_up(h, ts->lv[0], X, ldx, ts->nlev >= 1 ? ts->lv[1].in : ts->in_top,
-                  ts->nlev >= 1 ? ts->lv[1].rows : ts->cap, np, C, s));
+                  ts->nlev >= 1 ? ts->lv[1].rows : ts->cap, np, C, s, merge, mtoff));
   }
   {
     PROF(h, PQR_K_TSQR_TREE);
     for (int l = 1; l <= ts->nlev; ++l) {
       const bool root = l == ts->nlev;
       TRY(run_wy_up(h, ts->lv[l], ts->lv[l].in, ts->lv[l].rows, root ? ts->in_top : ts->lv[l + 1].in,
-                    root ? ts->cap : ts->lv[l + 1].rows, np, C, s));
+                    root ? ts->cap : ts->lv[l + 1].rows, np, C, s, merge, mtoff));
     }
   }
   if (h->comm) {
@@ -180,33 +183,34 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s) {
       CUDA_TRY(cudaMemcpy2DAsync(ts->xl.in + (int64_t)g * ts->cap, (size_t)ts->xl.rows * sizeof(double),
                                  ts->xraw + (int64_t)g * ts->cap * s, (size_t)ts->cap * sizeof(double),
                                  (size_t)ts->cap * sizeof(double), s, cudaMemcpyDeviceToDevice, h->stream));
-    TRY(run_wy_up(h, ts->xl, ts->xl.in, ts->xl.rows, ts->Btop, ts->cap, np, C, s));
+    TRY(run_wy_up(h, ts->xl, ts->xl.in, ts->xl.rows, ts->Btop, ts->cap, np, C, s, merge, mtoff));
   }
   return PQR_OK;
 }
 
 // Stage 2 over all levels: top coefficients cin (Call x ncol, ld cap) -> Y (n_local x ncol),
 // applying the first np panels.
-int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol, double* Y, int64_t ldy) {
+int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol, double* Y, int64_t ldy,
+                    const int4* pan) {
   TsqrState* ts = h->ts;
   const double* root_cin = cin;
   int64_t root_ld = ts->cap;
   {
     PROF(h, PQR_K_TSQR_TREE);
     if (h->comm) {
-      TRY(run_wy_down(h, ts->xl, cin, ts->cap, ts->xl.dn, ts->xl.rows, np, Call, t, ncol));
+      TRY(run_wy_down(h, ts->xl, cin, ts->cap, ts->xl.dn, ts->xl.rows, np, Call, t, ncol, pan));
       root_cin = ts->xl.dn + (int64_t)h->cfg.rank * ts->cap;
       root_ld = ts->xl.rows;
     }
     for (int l = ts->nlev; l >= 1; --l) {
       const bool root = l == ts->nlev;
       TRY(run_wy_down(h, ts->lv[l], root ? root_cin : ts->lv[l + 1].dn, root ? root_ld : ts->lv[l + 1].rows,
-                      ts->lv[l].dn, ts->lv[l].rows, np, Call, t, ncol));
+                      ts->lv[l].dn, ts->lv[l].rows, np, Call, t, ncol, pan));
     }
   }
   PROF(h, PQR_K_TSQR_APPLY);
   TRY(run_wy_down(h, ts->lv[0], ts->nlev >= 1 ? ts->lv[1].dn : root_cin, ts->nlev >= 1 ? ts->lv[1].rows : root_ld,
-                  Y, ldy, np, Call, t, ncol));
+                  Y, ldy, np, Call, t, ncol, pan));
   return PQR_OK;
 }
 
@@ -230,19 +234,28 @@ int run_top(Ctx* h, int s, bool build, double* P, int ldp, double* N, int ldn, i
 int tsqr_stage_panel(Ctx* h, int s) {
   TsqrState* ts = h->ts;
   const int np = (int)ts->panels.size();
-  const int2 pn = make_int2(ts->C, s);
-  CUDA_TRY(cudaMemcpyAsync(ts->d_pan + np, &pn, sizeof(int2), cudaMemcpyHostToDevice, h->stream));
+  const int4 pn = make_int4(ts->C, s, 16 * ts->C, 0);
+  CUDA_TRY(cudaMemcpyAsync(ts->d_pan + np, &pn, sizeof(int4), cudaMemcpyHostToDevice, h->stream));
   return PQR_OK;
 }
 
-// commit: R_top[:, k..k+t) = U~[0:C+s, 0:t);  panel (C, s) committed;  C += s  (k += t by the caller)
-int tsqr_commit(Ctx* h, int s, int t) {
+// commit: R_top[:, k..k+t) = U~[0:C+s, 0:t);  panel (C, s) committed — or, when the call
+// merged it into the previous panel, that panel widened to 8 with the merged T;  C += s
+// (k += t by the caller)
+int tsqr_commit(Ctx* h, int s, int t, int merge = 0, int mtoff = 0) {
   TsqrState* ts = h->ts;
   if (t > 0)
     CUDA_TRY(cudaMemcpy2DAsync(ts->Rt + (int64_t)h->k * ts->cap, ts->cap * sizeof(double), ts->Ut,
                                ts->cap * sizeof(double), (size_t)(ts->C + s) * sizeof(double), t,
                                cudaMemcpyDeviceToDevice, h->stream));
-  ts->panels.push_back(make_int2(ts->C, s));
+  if (merge) {
+    int4& pv = ts->panels.back();
+    pv = make_int4(pv.x, pv.y + s, mtoff, 1);
+    const int np = (int)ts->panels.size();
+    CUDA_TRY(cudaMemcpyAsync(ts->d_pan + np - 1, &pv, sizeof(int4), cudaMemcpyHostToDevice, h->stream));
+  } else {
+    ts->panels.push_back(make_int4(ts->C, s, 16 * ts->C, 0));
+  }
   ts->C += s;
   return PQR_OK;
 }
@@ -253,7 +266,7 @@ int alloc_level(Ctx* h, TsqrLv& lv, int wmax, bool with_io) {
   lv.UW = uw_for(lv.q + 2 * (lv.rem2 > 0) + lv.odd_last);
   lv.RP = rp_for(lv.UW);
   if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || wy_smem(lv.RP, wmax, ts->cap, 2) > (size_t)kSmemBudget) return PQR_EPLAN;
-  lv.tstride = (int64_t)16 * ts->cap;
+  lv.tstride = (int64_t)32 * ts->cap;  // [0, 16 cap): per-panel T at 16*start; then merged-pair T
   if (lv.owns_v && (rc = dalloc(&lv.V, (size_t)lv.rows * ts->cap))) return rc;
   if (lv.owns_v && with_io) CUDA_TRY(cudaMemsetAsync(lv.V, 0, sizeof(double) * lv.rows * ts->cap, h->stream));
   if ((rc = dalloc(&lv.T, (size_t)lv.nblocks * lv.tstride))) return rc;
@@ -316,7 +329,7 @@ int tsqr_alloc(Ctx* h) {
   if ((rc = dalloc(&ts->Rt, (size_t)cap * cap))) return rc;
   CUDA_TRY(cudaMemsetAsync(ts->Rt, 0, sizeof(double) * cap * cap, h->stream));
   if ((rc = dalloc(&ts->coef, (size_t)cap * 16))) return rc;
-  if ((rc = dalloc(&ts->d_pan, (size_t)cap + 1))) return rc;
+  if ((rc = dalloc(&ts->d_pan, (size_t)cap + 1)) || (rc = dalloc(&ts->d_panm, (size_t)cap + 1))) return rc;
   if (h->comm) {
     TsqrLv& x = ts->xl;
     x.nblocks = 1;
@@ -378,11 +391,30 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
     X = h->stageX;
     ldx = h->ld;
   }
-  TRY(tsqr_up_sweep(h, X, ldx, s));
+  // Narrow blocks (Arnoldi's s = 4): a 4-wide panel is merged with the previous 4-wide one
+  // into a full 8-wide panel (the up kernels build the merged T).
+  static const bool no_merge = getenv("PQR_NO_MERGE") != nullptr;
+  ts->merge = 0;
+  ts->mtoff = 0;
+  if (!no_merge && ts->wmax == 8 && np >= 1) {
+    const int4 pv = ts->panels.back();
+    if (pv.w == 0 && pv.y == 4 && s == 4 && pv.x + pv.y == ts->C) {
+      ts->merge = 1;
+      ts->mtoff = 16 * ts->cap + 16 * pv.x;
+    }
+  }
+  TRY(tsqr_up_sweep(h, X, ldx, s, ts->merge, ts->mtoff));
   TRY(run_top(h, s, false, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
-  TRY(tsqr_stage_panel(h, s));
   // U~ columns >= t are zero, so the down sweep writes zeros there.
-  TRY(tsqr_down_sweep(h, np + 1, ts->C + s, ts->Ut, s, s, Ud, ldud));
+  if (ts->merge) {
+    std::vector<int4> lst(ts->panels);
+    lst.back() = make_int4(lst.back().x, 8, ts->mtoff, 1);
+    CUDA_TRY(cudaMemcpyAsync(ts->d_panm, lst.data(), sizeof(int4) * np, cudaMemcpyHostToDevice, h->stream));
+    TRY(tsqr_down_sweep(h, np, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_panm));
+  } else {
+    TRY(tsqr_stage_panel(h, s));
+    TRY(tsqr_down_sweep(h, np + 1, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_pan));
+  }
   // t reaches the host with the caller's single synchronisation; the caller commits the
   // panel (tsqr_commit) once t is known and the call has not failed
   CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -418,7 +450,7 @@ int tsqr_apply(Ctx* h, const double* C, int ldc, int m, double* Y, int64_t ldy) 
         TRY(run_update(ts->C, k, ts->Rt, ts->cap, 0, nullptr, 0, h->stageC, k, mc, nullptr, ts->coef, ts->cap,
                        nullptr, 0, h->sms, h->stream, &h->st.kernel_launches));
       }
-      TRY(tsqr_down_sweep(h, np, ts->C, ts->coef, mc, mc, dst, ldd));
+      TRY(tsqr_down_sweep(h, np, ts->C, ts->coef, mc, mc, dst, ldd, ts->d_pan));
     }
     if (stage)
       CUDA_TRY(cudaMemcpy2DAsync(Y + (int64_t)c0 * ldy, ldy * sizeof(double), h->stageU, h->ld * sizeof(double),
@@ -449,6 +481,7 @@ void tsqr_free(Ctx* h) {
   cudaFree(ts->Rt);
   cudaFree(ts->coef);
   cudaFree(ts->d_pan);
+  cudaFree(ts->d_panm);
   delete ts;
   h->ts = nullptr;
 }

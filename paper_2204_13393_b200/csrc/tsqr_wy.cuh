@@ -67,7 +67,7 @@ struct WyLevel {
 };
 
 struct WyPanels {
-  const int2* pan;  // (start, width) per panel, device
+  const int4* pan;  // (start, width, T offset in the block's T area, merged) per panel, device
   int np;           // panels to apply
 };
 
@@ -80,11 +80,12 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
 inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
   const size_t E = (size_t)wmax * wmax;
   return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 512) * sizeof(double) +
-         (size_t)((cap + 2) & ~1) * sizeof(int2) + (size_t)2 * nbuf * sizeof(uint64_t);
+         (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
 template <int UW, int NT, bool UP>
-PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol) {
+PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge,
+                     int mtoff) {
   extern __shared__ __align__(16) double sm[];
   const int RP = L.RP, wm = L.wmax, nbuf = L.nbuf;
   const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
@@ -95,8 +96,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   double* hred = Zs + E;                   // 2 x (kWyWarps*16 partials + 16 pivot-row values)
   double* diagv = hred + kWyHH;            // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
-  int2* pans = reinterpret_cast<int2*>(tsc + 512);
-  uint64_t* full = reinterpret_cast<uint64_t*>(pans + ((L.cap + 2) & ~1));
+  int4* pans = reinterpret_cast<int4*>(tsc + 512);
+  uint64_t* full = reinterpret_cast<uint64_t*>(pans + L.cap + 2);
   uint64_t* empty = full + nbuf;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -142,13 +143,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             for (int c = 0; c < s; ++c)
               bulk_g2s(buf + c * RP, L.X + r0 + (int64_t)c * L.ldx, (uint32_t)Re * 8u, bar);
         } else {
-          const int2 pn = pans[UP ? p - 1 : np - 1 - p];
+          const int4 pn = pans[UP ? p - 1 : np - 1 - p];
           const int Rc = R + (R & 1);  // includes the zero pad row of an odd block
           const uint32_t tb = (uint32_t)((pn.y * pn.y + 1) & ~1) * 8u;
           mbar_arrive_expect_tx(bar, (uint32_t)pn.y * Rc * 8u + tb);
           for (int j = 0; j < pn.y; ++j)
             bulk_g2s(buf + j * RP, L.V + (int64_t)(pn.x + j) * L.ldv + r0, (uint32_t)Rc * 8u, bar);
-          bulk_g2s(buf + RP * wm, L.T + b * L.tstride + 16 * pn.x, tb, bar);
+          bulk_g2s(buf + RP * wm, L.T + b * L.tstride + pn.z, tb, bar);
         }
       }
     }
@@ -325,7 +326,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           }
         }
       }
-      release(it);
+      if (!(UP && merge && p == np - 1)) release(it);  // merging: the last panel stays for the tail
       WY_TR(6);
       if (mrow) {  // rows >= R stay zero (stale slot rows may be non-zero)
 #pragma unroll
@@ -507,6 +508,78 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
     }
     __syncwarp();
+    if (merge) {
+      // The previous panel (width w1, still in its slot) and the new one (s = 8 - w1) become
+      // one 8-wide panel: H_prev H_new = I - [V1 V2] [T1, -T1 (V1^T V2) T2; 0, T2] [V1 V2]^T.
+      // V1^T V2 takes one more reduction (lane-local products in the row layout).
+      const int64_t hit = it - 1;  // the held item
+      const double* v1 = ring + (size_t)(hit % nbuf) * SS;
+      constexpr int w1 = 4;  // merges pair two 4-wide panels (host: s == 4 after a 4-wide panel)
+      const double* T1 = v1 + RP * wm;
+      double Dp[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) Dp[i] = 0.0;
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        const int row = rowk[e];
+#pragma unroll
+        for (int j = 0; j < w1; ++j) {
+          const double a1 = v1[j * RP + row];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double v2 = row >= C + c ? xr[e][c] : 0.0;
+            Dp[j * 4 + c] = fma(a1, v2, Dp[j * 4 + c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int mb = 16, w = 16; w > 1; mb >>= 1, w >>= 1) {
+        const bool up = (lane & mb) != 0;
+#pragma unroll
+        for (int j = 0; j < w / 2; ++j) {
+          const double send = up ? Dp[j] : Dp[j + w / 2];
+          const double keep = up ? Dp[j + w / 2] : Dp[j];
+          Dp[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
+        }
+      }
+      Dp[0] += __shfl_xor_sync(0xffffffffu, Dp[0], 1);
+      double* hb = hred + hpar * (kWyWarps * kWyHS + 16);
+      hpar ^= 1;
+      if ((lane & 1) == 0) hb[warp * kWyHS + ((lane >> 1) & 15)] = Dp[0];
+      cbar();
+      if (warp == 0) {
+        // C = V1^T V2 (w1 x s, entry j*s + c): lane l sums value l & 15 over 8 warps, xor 16
+        const int v = lane & 15, part = lane >> 4;
+        double tot = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) tot += hb[(part * 8 + ww) * kWyHS + v];
+        tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+        double* Cm = tsc + 256 + 16 * 8;  // 16 scratch words after the T columns (s <= 8 here)
+        if (lane < 16) Cm[lane] = tot;
+        __syncwarp();
+        // T_m (8 x 8, ld 8): [T1, -T1 C T2; 0, T2]; T2 column c = col scratch of thread c
+        double* Tm = L.T + b * L.tstride + mtoff;
+        for (int e2 = lane; e2 < 64; e2 += 32) {
+          const int i = e2 & 7, jj = e2 >> 3;
+          double val = 0.0;
+          if (i < w1 && jj < w1) {
+            val = i <= jj ? T1[i + w1 * jj] : 0.0;
+          } else if (i >= w1 && jj >= w1) {
+            const int i2 = i - w1, j2 = jj - w1;
+            val = i2 <= j2 ? tsc[256 + 16 * j2 + i2] : 0.0;
+          } else if (i < w1 && jj >= w1) {
+            const int j2 = jj - w1;
+            for (int a = i; a < w1; ++a) {
+              double cta = 0.0;  // (C T2)[a][j2]
+              for (int bb = 0; bb <= j2; ++bb) cta += Cm[a * s + bb] * tsc[256 + 16 * j2 + bb];
+              val -= T1[i + w1 * a] * cta;
+            }
+          }
+          Tm[i + 8 * jj] = val;
+        }
+      }
+      release(hit);
+    }
     WY_TR(8);
     // ---------------- outputs: [P_b; N_b] to the parent slot, the new reflectors ----------------
     {
@@ -534,14 +607,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 }
 
 template <int UW, int NT>
-__global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s) {
-  wy_body<UW, NT, true>(L, P, C, s, 0, 0);
+__global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
+  wy_body<UW, NT, true>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
 template <int UW, int NT>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  wy_body<UW, NT, false>(L, P, 0, t, Call, ncol);
+  wy_body<UW, NT, false>(L, P, 0, t, Call, ncol, 0, 0);
 }
 
 }  // namespace pqr

@@ -202,26 +202,28 @@ def test_capacity_error(P, variant):
         assert e.value.code == P.PQR_ECAPACITY
 
 
+@pytest.mark.parametrize("widths,probe", [([8, 3, 8, 5], 8), ([4, 4, 4, 4, 8, 4, 4], 4)])
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_mixed_block_widths_and_no_append(P, orc, variant):
+def test_mixed_block_widths_and_no_append(P, orc, variant, widths, probe):
     """A sequence with varying s and NO_APPEND probes in between (the Arnoldi pattern when a
     block deflates): every solve matches the oracle on the basis accumulated so far.  Covers
-    TSQR panels of different widths in one LOR and stale tree-slot rows after a wider probe."""
+    TSQR panels of different widths in one LOR, stale tree-slot rows after a wider probe, and
+    the merge of consecutive 4-wide panels into 8-wide ones (committed and probed)."""
     import torch
 
     n, k0 = 70_001, 13  # several leaf blocks per CTA, odd n (pad row), odd k0
     Q = inputs.orthonormal(101, n, k0)
     basis = Q.copy(order="F")
-    widths = [8, 3, 8, 5]
     with P.PQR(n, k0 + sum(widths), 8, dev(Q), variant=variant) as h:
         for i, s in enumerate(widths):
-            # a wider probe that must leave no trace, then the real (appending) solve
-            Xp = inputs.gaussian(200 + i, n, 8)
-            Up, Pp, Np = empty(n, 8), empty(basis.shape[1], 8), empty(8, 8)
-            tp = h.solve(dev(Xp), U=Up, P=Pp, N=Np, flags=P.PQR_NO_APPEND)
+            # a probe that must leave no trace (4-wide probes exercise the TSQR panel merge
+            # without committing it), then the real (appending) solve
+            Xp = inputs.gaussian(200 + i, n, probe)
+            Up, Pp, Np = empty(n, probe), empty(basis.shape[1], probe), empty(probe, probe)
+            tp = h.solve(dev(Xp), U=Up, P=Pp, N=Np, flags=P.PQR_NO_APPEND, s=probe)
             torch.cuda.synchronize()
             refp = orc.householder_pqr(basis, Xp)
-            assert tp == refp["t"] == 8
+            assert tp == refp["t"] == probe
             assert rel(host(Pp), refp["P"]) < 1e-10 and rel(host(Up)[:, :tp], refp["U"]) < 1e-10
             X = inputs.gaussian(300 + i, n, s)
             U, Pm, Nm = empty(n, s), empty(basis.shape[1], s), empty(s, s)
