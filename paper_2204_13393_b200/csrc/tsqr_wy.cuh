@@ -286,14 +286,38 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       WY_TR(4);
       cbar();  // B2: Z complete
       WY_TR(5);
-      // Z'^T = Z^T T (stage 1) or Z^T T^T (stage 2): lane gets Z'[8jt+2q+v][8nt+g]
+      // Z'^T = Z^T T (stage 1) or Z^T T^T (stage 2): lane gets Z'[8jt+2q+v][8nt+g].
+      // 8-wide panels: every warp forms it (two MMAs).  16-wide panels: warps 0-3 form one
+      // 8x8 tile each into shared memory (tsc: free outside the stage-1 tail) behind one
+      // more barrier, instead of 16 MMAs in every warp.
       double zp[NT][2][2];
+      const bool shared_zp = NT > 1 && mtn == 2;
+      if (shared_zp) {
+        if (warp < 4) {
+          const int jt = warp >> 1, nt = warp & 1, jj = 8 * jt + g;
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int l = 4 * k4 + q;
+            const double a = Zs[l + wm * (8 * nt + g)];
+            const double bt = (l < w && jj < w) ? (UP ? Tg[l + w * jj] : Tg[jj + w * l]) : 0.0;
+            dmma884(d0, d1, a, bt);
+          }
+          // D[m = c = 8nt+g][n = j = 8jt+2q+v]: store Z'[j][c] at tsc[j + 16 c]
+          tsc[(8 * jt + 2 * q) + 16 * (8 * nt + g)] = d0;
+          tsc[(8 * jt + 2 * q + 1) + 16 * (8 * nt + g)] = d1;
+        }
+        cbar();
+      }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int jt = 0; jt < 2; ++jt) {
           zp[nt][jt][0] = zp[nt][jt][1] = 0.0;
-          if (jt < mtn) {
+          if (shared_zp) {
+            zp[nt][jt][0] = tsc[(8 * jt + 2 * q) + 16 * (8 * nt + g)];
+            zp[nt][jt][1] = tsc[(8 * jt + 2 * q + 1) + 16 * (8 * nt + g)];
+          } else if (jt < mtn) {
             const int jj = 8 * jt + g;
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4) {
