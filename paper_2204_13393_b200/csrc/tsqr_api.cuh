@@ -57,9 +57,19 @@ int nbuf_for(int RP, int wmax, int cap) {
 template <int UW, int NT>
 cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
                     cudaStream_t st) {
-  auto f = k_wy_up<UW, NT>;
-  ensure_smem(f, smem);
-  f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
+  if constexpr (NT == 1) {  // panel merges only pair 4-wide panels (s = 4)
+    if (merge) {
+      auto f = k_wy_up<UW, NT, true>;
+      ensure_smem(f, smem);
+      f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
+      return cudaGetLastError();
+    }
+  }
+  {
+    auto f = k_wy_up<UW, NT, false>;
+    ensure_smem(f, smem);
+    f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, 0, 0);
+  }
   return cudaGetLastError();
 }
 template <int UW, int NT>

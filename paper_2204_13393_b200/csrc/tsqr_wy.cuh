@@ -83,9 +83,11 @@ inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
          (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
-template <int UW, int NT, bool UP>
-PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge,
+template <int UW, int NT, bool UP, bool MERGE = false>
+PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge_,
                      int mtoff) {
+  constexpr bool merge = MERGE;  // separate instantiation: the common path carries no merge code
+  (void)merge_;
   extern __shared__ __align__(16) double sm[];
   const int RP = L.RP, wm = L.wmax, nbuf = L.nbuf;
   const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
@@ -532,7 +534,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       for (int i = 0; i < s; ++i) Tn[i + c * s] = i <= c ? col[i] : 0.0;
     }
     __syncwarp();
-    if (merge) {
+    if constexpr (merge) {
       // The previous panel (width w1, still in its slot) and the new one (s = 8 - w1) become
       // one 8-wide panel: H_prev H_new = I - [V1 V2] [T1, -T1 (V1^T V2) T2; 0, T2] [V1 V2]^T.
       // V1^T V2 takes one more reduction (lane-local products in the row layout).
@@ -630,9 +632,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #undef WY_TR
 }
 
-template <int UW, int NT>
+template <int UW, int NT, bool MERGE>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<UW, NT, true>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<UW, NT, true, MERGE>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
