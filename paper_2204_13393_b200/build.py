@@ -30,7 +30,8 @@ def deps():
     return sorted(glob.glob(os.path.join(CSRC, "*")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True compiles the TSQR phase counters in (PQR_WY_TRACE=1 then prints them)."""
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps()):
@@ -39,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3",
-           "-I", inc, "-I", os.path.join(ROOT, "include"),
+           "-I", inc, "-I", os.path.join(ROOT, "include"), *(["-DPQR_WY_TRACE"] if trace else []),
            *sources(), "-o", tmp,
            "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}", "-lcudart"]
     subprocess.check_call(cmd)
@@ -48,4 +49,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -182,7 +182,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     }
     if (rz_part == 0) Zs[rz_e] = z;
   };
-  // optional phase tracing (CTA 0, warps 0 and 15, lane 0): cycles per phase in smem
+  // optional phase tracing (CTA 0, warps 0 and 15, lane 0): cycles per phase in smem.
+  // Compiled in only with -DPQR_WY_TRACE (tools: build.py --trace); absent from the product build.
+#ifdef PQR_WY_TRACE
   __shared__ unsigned long long s_tr[2][16];
   const bool tr_on = L.trace != nullptr && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kWyWarps - 1);
   const int tr_w = warp == 0 ? 0 : 1;
@@ -197,6 +199,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     s_tr[tr_w][k] += (unsigned long long)(t1_ - tr_t0); \
     tr_t0 = t1_;                                       \
   }
+#else
+#define WY_TR(k)
+#endif
 
   int64_t it = 0;  // consumer item cursor
   int hpar = 0;    // Householder-round buffer parity
@@ -627,8 +632,10 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     }  // stage-1 tail
   }
   WY_TR(9);
+#ifdef PQR_WY_TRACE
   if (tr_on)
     for (int i = 0; i < 16; ++i) L.trace[tr_w * 16 + i] = s_tr[tr_w][i];
+#endif
 #undef WY_TR
 }
 
