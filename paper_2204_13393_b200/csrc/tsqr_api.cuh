@@ -54,38 +54,39 @@ int nbuf_for(int RP, int wmax, int cap) {
   return 2;
 }
 
-template <int UW, int NT>
+template <int UW, int NT, int WM>
 cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
                     cudaStream_t st) {
-  if constexpr (NT == 1) {  // panel merges only pair 4-wide panels (s = 4)
+  if constexpr (NT == 1 && WM == 8) {  // panel merges only pair 4-wide panels (s = 4)
     if (merge) {
-      auto f = k_wy_up<UW, NT, true>;
+      auto f = k_wy_up<UW, NT, WM, true>;
       ensure_smem(f, smem);
       f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
       return cudaGetLastError();
     }
   }
-  {
-    auto f = k_wy_up<UW, NT, false>;
-    ensure_smem(f, smem);
-    f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, 0, 0);
-  }
+  auto f = k_wy_up<UW, NT, WM, false>;
+  ensure_smem(f, smem);
+  f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, 0, 0);
   return cudaGetLastError();
 }
-template <int UW, int NT>
+template <int UW, int NT, int WM>
 cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
                       cudaStream_t st) {
-  auto f = k_wy_down<UW, NT>;
+  auto f = k_wy_down<UW, NT, WM>;
   ensure_smem(f, smem);
   f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
   return cudaGetLastError();
 }
 
-#define PQR_WY_SWITCH(UW_, NT_, CALL)                                                        \
-  switch ((UW_) * 10 + (NT_)) {                                                              \
-    case 21: e = CALL(2, 1); break; case 22: e = CALL(2, 2); break;                         \
-    case 41: e = CALL(4, 1); break;                                                          \
-    case 61: e = CALL(6, 1); break;                                                          \
+// (UW, NT, WM) instantiations: WM = 16 levels have UW <= 2 (alloc_level)
+#define PQR_WY_SWITCH(UW_, NT_, WM_, CALL)                                                   \
+  switch ((UW_) * 100 + (NT_) * 10 + ((WM_) > 8 ? 1 : 0)) {                                  \
+    case 210: e = CALL(2, 1, 8); break;                                                      \
+    case 410: e = CALL(4, 1, 8); break;                                                      \
+    case 610: e = CALL(6, 1, 8); break;                                                      \
+    case 211: e = CALL(2, 1, 16); break;                                                     \
+    case 221: e = CALL(2, 2, 16); break;                                                     \
     default: return PQR_EPLAN;                                                               \
   }
 
@@ -126,8 +127,8 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
   const int grid = std::min(lv.nblocks, h->sms);
   cudaError_t e;
-#define UPC(U, N) wy_up_t<U, N>(L, P, C, s, merge, mtoff, grid, smem, h->stream)
-  PQR_WY_SWITCH(lv.UW, NT, UPC)
+#define UPC(U, N, W) wy_up_t<U, N, W>(L, P, C, s, merge, mtoff, grid, smem, h->stream)
+  PQR_WY_SWITCH(lv.UW, NT, ts->wmax, UPC)
 #undef UPC
   wy_trace_dump("up", L, h->stream);
   ++h->st.kernel_launches;
@@ -149,8 +150,8 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
   const int grid = std::min(lv.nblocks, h->sms);
   cudaError_t e;
-#define DNC(U, N) wy_down_t<U, N>(L, P, Call, t, ncol, grid, smem, h->stream)
-  PQR_WY_SWITCH(lv.UW, NT, DNC)
+#define DNC(U, N, W) wy_down_t<U, N, W>(L, P, Call, t, ncol, grid, smem, h->stream)
+  PQR_WY_SWITCH(lv.UW, NT, ts->wmax, DNC)
 #undef DNC
   wy_trace_dump("down", L, h->stream);
   ++h->st.kernel_launches;

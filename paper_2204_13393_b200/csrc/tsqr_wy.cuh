@@ -83,13 +83,14 @@ inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
          (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
-template <int UW, int NT, bool UP, bool MERGE = false>
+template <int UW, int NT, int WM, bool UP, bool MERGE = false>
 PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge_,
                      int mtoff) {
   constexpr bool merge = MERGE;  // separate instantiation: the common path carries no merge code
   (void)merge_;
   extern __shared__ __align__(16) double sm[];
-  const int RP = L.RP, wm = L.wmax, nbuf = L.nbuf;
+  constexpr int wm = WM, MTM = WM / 8;  // widest panel (8 or 16) and its 8-column tiles
+  const int RP = L.RP, nbuf = L.nbuf;
   const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
   const int E = wm * wm;
   double* ring = sm;
@@ -253,15 +254,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       const int w = pans[UP ? p : np - 1 - p].y;
       const int mtn = (w + 7) >> 3;
       // Z = V^T x: per-warp partials, two accumulator chains over alternate units
-      double acc[2][2][NT][2];
+      double acc[2][MTM][NT][2];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MTM; ++mt)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) acc[h][mt][nt][0] = acc[h][mt][nt][1] = 0.0;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < MTM; ++mt) {
         if (mt < mtn) {
 #pragma unroll
           for (int u = 0; u < UW; ++u) {
@@ -297,9 +298,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       // 8-wide panels: every warp forms it (two MMAs).  16-wide panels: warps 0-3 form one
       // 8x8 tile each into shared memory (tsc: free outside the stage-1 tail) behind one
       // more barrier, instead of 16 MMAs in every warp.
-      double zp[NT][2][2];
+      double zp[NT][MTM][2];
       const bool shared_zp = NT > 1 && mtn == 2;
-      if (shared_zp) {
+      if (MTM == 2 && shared_zp) {
         if (warp < 4) {
           const int jt = warp >> 1, nt = warp & 1, jj = 8 * jt + g;
           double d0 = 0.0, d1 = 0.0;
@@ -319,15 +320,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int jt = 0; jt < 2; ++jt) {
+        for (int jt = 0; jt < MTM; ++jt) {
           zp[nt][jt][0] = zp[nt][jt][1] = 0.0;
-          if (shared_zp) {
+          if (MTM == 2 && shared_zp) {
             zp[nt][jt][0] = tsc[(8 * jt + 2 * q) + 16 * (8 * nt + g)];
             zp[nt][jt][1] = tsc[(8 * jt + 2 * q + 1) + 16 * (8 * nt + g)];
           } else if (jt < mtn) {
             const int jj = 8 * jt + g;
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4) {
+            for (int k4 = 0; k4 < 2 * MTM; ++k4) {
               if (k4 < 2 * mtn) {
                 const int l = 4 * k4 + q;
                 const double a = Zs[l + wm * (8 * nt + g)];
@@ -339,7 +340,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         }
       // x^T -= Z'^T V^T
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < 2 * MTM; ++kk) {
         if (kk < 2 * mtn) {
           const int j = 8 * (kk >> 1) + 2 * q + (kk & 1);
           double am[NT];
@@ -639,15 +640,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #undef WY_TR
 }
 
-template <int UW, int NT, bool MERGE>
+template <int UW, int NT, int WM, bool MERGE>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<UW, NT, true, MERGE>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<UW, NT, WM, true, MERGE>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
-template <int UW, int NT>
+template <int UW, int NT, int WM>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  wy_body<UW, NT, false>(L, P, 0, t, Call, ncol, 0, 0);
+  wy_body<UW, NT, WM, false>(L, P, 0, t, Call, ncol, 0, 0);
 }
 
 }  // namespace pqr
