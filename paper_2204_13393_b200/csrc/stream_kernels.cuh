@@ -348,12 +348,13 @@ __global__ void __launch_bounds__(kCpaThreads, NT == 1 ? 2 : 1) k_update_gram_cp
     double d[NT][2][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) d[nt][0][0] = d[nt][0][1] = d[nt][1][0] = d[nt][1][1] = 0.0;
-    // k-steps past this warp's quarter have zero M fragments (mreg); their stage reads stay
-    // inside the shared allocation (next stage or sMm: finite), so no predicate is needed
+    // k-steps past this warp's quarter have zero M fragments (mreg) and read a clamped, valid
+    // column of the stage (finite data), so no predicate is needed
 #pragma unroll
     for (int i = 0; i < MTH; ++i) {
       {
-        const double2 av = lds2(buf + (4 * (kk0 + i) + q) * kFuseRBP + 16 * uu + 2 * gq);
+        const int kc = min(kk0 + i, KS - 1);
+        const double2 av = lds2(buf + (4 * kc + q) * kFuseRBP + 16 * uu + 2 * gq);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           dmma884(d[nt][0][0], d[nt][0][1], mreg[i][nt], av.x);
