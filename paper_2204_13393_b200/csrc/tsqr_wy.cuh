@@ -79,7 +79,7 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
 // shared-memory bytes of a level kernel (host and device agree on this layout)
 inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
   const size_t E = (size_t)wmax * wmax;
-  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 512) * sizeof(double) +
+  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 512 + 64) * sizeof(double) +
          (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
@@ -99,7 +99,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   double* hred = Zs + E;                   // 2 x (kWyWarps*16 partials + 16 pivot-row values)
   double* diagv = hred + kWyHH;            // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
-  int4* pans = reinterpret_cast<int4*>(tsc + 512);
+  double* hfc = tsc + 512;                 // 2 x 32: Householder-round coefficients (by round parity)
+  int4* pans = reinterpret_cast<int4*>(hfc + 64);
   uint64_t* full = reinterpret_cast<uint64_t*>(pans + L.cap + 2);
   uint64_t* empty = full + nbuf;
 
@@ -482,44 +483,49 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       WY_TR(11);
       cbar();
       WY_TR(12);
-      // sums over the 16 warps (lane: value lane % S8, a quarter/half of the warps), broadcast
-      double tot;
-      {
+      // Warp 0 alone sums the 16 warp partials, forms the reflector scalars (one sqrt/rsqrt
+      // chain per CTA) and the update coefficients, and publishes them behind a second barrier
+      // (cheaper than every warp reducing and broadcasting the totals itself).
+      double* hf = hfc + (c & 1) * 32;  // [0, S8): coefficients; S8: inv; S8+1: u0 - sigma*lambda
+      if (warp == 0) {
         constexpr int NP = 32 / S8, WPP = kWyWarps / NP;  // lane groups, warps per group
         const int v = lane & (S8 - 1), part = lane / S8;
         const double* hv = hb + part * WPP * kWyHS + v;
-        tot = 0.0;
+        double tot = 0.0;
 #pragma unroll
         for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
 #pragma unroll
         for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
+        const double lam2 = __shfl_sync(0xffffffffu, tot, c);
+        const double u0 = hb[kWyWarps * kWyHS + c];
+        const double lam = sqrt(lam2);
+        const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
+        const double diag = sigma * lam;
+        const double nv2 = 2.0 * lam * (lam + fabs(u0));
+        const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
+        // v . x_v (v > c: update coefficient / 2) and v_v . v_c (v < c: column c of V^T V)
+        const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[kWyWarps * kWyHS + v]);
+        if (lane < S8) {
+          hf[lane] = fv;
+          if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
+        }
+        if (lane == 0) {
+          hf[S8] = inv;
+          hf[S8 + 1] = u0 - diag;
+          diagv[c] = diag;
+        }
       }
       WY_TR(14);
-      double Dt[S8];
-#pragma unroll
-      for (int cc = 0; cc < S8; ++cc) Dt[cc] = __shfl_sync(0xffffffffu, tot, cc);
-      const double u0 = hb[kWyWarps * kWyHS + c];
+      cbar();
       WY_TR(15);
-      const double lam = sqrt(Dt[c]);
-      const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
-      const double diag = sigma * lam;
-      const double nv2 = 2.0 * lam * (lam + fabs(u0));
-      const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
-      double f[S8];
-#pragma unroll
-      for (int cc = 0; cc < S8; ++cc) f[cc] = cc == c ? 0.0 : 2.0 * inv * (Dt[cc] - diag * hb[kWyWarps * kWyHS + cc]);
-      if (tid == 0) {
-        diagv[c] = diag;
-#pragma unroll
-        for (int cc = 0; cc < c; ++cc) Gs[cc + 16 * c] = 0.5 * f[cc];  // v_cc . v_c
-      }
+      const double inv = hf[S8], wr = hf[S8 + 1];
       WY_TR(13);
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
         if (rowk[e] >= r) {
-          const double vv = (rowk[e] == r ? u0 - diag : xr[e][c]) * inv;
+          const double vv = (rowk[e] == r ? wr : xr[e][c]) * inv;
 #pragma unroll
-          for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-f[cc], vv, xr[e][cc]);
+          for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-hf[cc], vv, xr[e][cc]);
           xr[e][c] = vv;
         }
     }
