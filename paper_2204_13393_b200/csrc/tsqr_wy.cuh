@@ -254,6 +254,66 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       const double* Tg = vb + RP * wm;
       const int w = pans[UP ? p : np - 1 - p].y;
       const int mtn = (w + 7) >> 3;
+      double zp[NT][MTM][2];
+      if constexpr (MTM == 1 && !UP) {
+        // 8-wide panels, stage 2 (measured: slower in stage 1, whose kernel carries the
+        // Householder tail): each warp forms its partial of Z^T = x^T V (A = x from registers,
+        // B = V from the slot) and multiplies it by T (stage 1) or T^T (stage 2) right away, so
+        // the summed partials are Z'^T itself; after the barriers a lane only loads the two
+        // coefficients it needs (no per-warp MMA chain between the second barrier and the update)
+        double acc[2][NT][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          const int row = 16 * (warp * UW + u) + 4 * q;
+          const double* vp = vb + g * RP + row;
+          const double2 a01 = *reinterpret_cast<const double2*>(vp);
+          const double2 a23 = *reinterpret_cast<const double2*>(vp + 2);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            double (&ac)[2] = acc[u & 1][nt];
+            dmma884(ac[0], ac[1], x[u][nt][0], a01.x);
+            dmma884(ac[0], ac[1], x[u][nt][1], a01.y);
+            dmma884(ac[0], ac[1], x[u][nt][2], a23.x);
+            dmma884(ac[0], ac[1], x[u][nt][3], a23.y);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double p0 = acc[0][nt][0] + acc[1][nt][0];  // Z^T[c = 8nt+g][j = 2q]
+          const double p1 = acc[0][nt][1] + acc[1][nt][1];  // Z^T[c][2q + 1]
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int k4 = 0; k4 < 2; ++k4) {
+            const int src = 4 * g + 2 * k4 + (q >> 1);  // holder of Z^T[c][l = 4 k4 + q]
+            const double s0 = __shfl_sync(0xffffffffu, p0, src);
+            const double s1 = __shfl_sync(0xffffffffu, p1, src);
+            const int l = 4 * k4 + q;
+            const double bt = (l < w && g < w) ? (UP ? Tg[l + w * g] : Tg[g + w * l]) : 0.0;
+            dmma884(d0, d1, (q & 1) ? s1 : s0, bt);
+          }
+          // D[c = 8nt+g][j = 2q + v] of this warp's partial of Z'^T
+          red[((2 * q) + wm * (8 * nt + g)) * (kWyWarps + 1) + warp] = d0;
+          red[((2 * q + 1) + wm * (8 * nt + g)) * (kWyWarps + 1) + warp] = d1;
+        }
+        WY_TR(1);
+        cbar();  // B1: partials complete; every warp is done with the previous item
+        WY_TR(2);
+        WY_TR(3);
+        reduce_Z();
+        WY_TR(4);
+        cbar();  // B2: Z'^T complete
+        WY_TR(5);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double2 z2 = *reinterpret_cast<const double2*>(Zs + 2 * q + wm * (8 * nt + g));
+          zp[nt][0][0] = z2.x;
+          zp[nt][0][1] = z2.y;
+        }
+      } else {
       // Z = V^T x: per-warp partials, two accumulator chains over alternate units
       double acc[2][MTM][NT][2];
 #pragma unroll
@@ -299,7 +359,6 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       // 8-wide panels: every warp forms it (two MMAs).  16-wide panels: warps 0-3 form one
       // 8x8 tile each into shared memory (tsc: free outside the stage-1 tail) behind one
       // more barrier, instead of 16 MMAs in every warp.
-      double zp[NT][MTM][2];
       const bool shared_zp = NT > 1 && mtn == 2;
       if (MTM == 2 && shared_zp) {
         if (warp < 4) {
@@ -339,6 +398,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             }
           }
         }
+      }
       // x^T -= Z'^T V^T
 #pragma unroll
       for (int kk = 0; kk < 2 * MTM; ++kk) {
