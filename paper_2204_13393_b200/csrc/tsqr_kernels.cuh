@@ -86,11 +86,28 @@ __global__ void __launch_bounds__(256) k_tsqr_top(TsqrTopArgs a) {
   __syncthreads();
   // ---- P = R_top^T B, B -= R_top P  (twice: BCGS+ against the orthonormal R_top) ----
   for (int pass = 0; pass < 2 && k > 0; ++pass) {
-    for (int e = tid; e < k * s; e += blockDim.x) {
-      const int i = e % k, c = e / k;
-      double acc = 0.0;
-      for (int r = 0; r < C; ++r) acc += a.Rt[r + (int64_t)i * a.ldr] * sB[r + c * kTopMaxRows];
-      sV[e] = acc;  // scratch
+    {  // P_pass = R_top^T B: one warp per column i of R_top, lanes over its rows (coalesced)
+      const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+      for (int i = warp; i < k; i += nw) {
+        double acc[kSMaxTop];
+#pragma unroll
+        for (int c = 0; c < kSMaxTop; ++c) acc[c] = 0.0;
+        for (int r = lane; r < C; r += 32) {
+          const double rv = a.Rt[r + (int64_t)i * a.ldr];
+#pragma unroll
+          for (int c = 0; c < kSMaxTop; ++c)
+            if (c < s) acc[c] = fma(rv, sB[r + c * kTopMaxRows], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < kSMaxTop; ++c) {
+          if (c < s) {
+            double v = acc[c];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) sV[i + c * k] = v;  // scratch
+          }
+        }
+      }
     }
     __syncthreads();
     for (int e = tid; e < C * s; e += blockDim.x) {
