@@ -367,12 +367,23 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
   h->k = 0;
   ts->C = 0;
   const int chunk = ts->wmax;
-  double* Qal = nullptr;  // 16-byte aligned copy with even ld for the bulk copies
+  // 16-byte aligned copy of Q with even ld for the bulk copies (freed on every exit path)
+  struct AlignedQ {
+    double* p = nullptr;
+    cudaStream_t st = nullptr;
+    ~AlignedQ() {
+      if (p) {
+        cudaStreamSynchronize(st);
+        cudaFree(p);
+      }
+    }
+  } qa;
+  qa.st = h->stream;
   if (k > 0 && ((ldq & 1) || !aligned16(Q))) {
-    TRY(dalloc(&Qal, (size_t)h->ld * k));
-    CUDA_TRY(cudaMemcpy2DAsync(Qal, h->ld * sizeof(double), Q, ldq * sizeof(double),
+    TRY(dalloc(&qa.p, (size_t)h->ld * k));
+    CUDA_TRY(cudaMemcpy2DAsync(qa.p, h->ld * sizeof(double), Q, ldq * sizeof(double),
                                h->cfg.n_local * sizeof(double), k, cudaMemcpyDeviceToDevice, h->stream));
-    Q = Qal;
+    Q = qa.p;
     ldq = h->ld;
   }
   for (int c0 = 0; c0 < k; c0 += chunk) {
@@ -382,10 +393,6 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
     TRY(tsqr_stage_panel(h, cs));
     TRY(tsqr_commit(h, cs, cs));
     h->k += cs;
-  }
-  if (Qal) {
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
-    cudaFree(Qal);
   }
   return PQR_OK;
 }
