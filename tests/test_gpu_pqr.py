@@ -235,3 +235,21 @@ def test_mixed_block_widths_and_no_append(P, orc, variant, widths, probe):
             assert rel(host(U)[:, :t], ref["U"]) < 1e-10
             basis = np.asfortranarray(np.hstack([basis, ref["U"]]))
         assert h.k == basis.shape[1]
+
+
+def test_tsqr_invalid_block_plan(P):
+    """Leaf blocks larger than the level kernels hold (6 x 256 rows per CTA) are refused with
+    PQR_EPLAN (SPEC InvalidPlan), not run."""
+    import torch
+
+    n = 100_000
+    Q = dev(inputs.orthonormal(5, n, 8))
+    with pytest.raises(P.PQRError) as e:
+        P.PQR(n, 16, 8, Q, variant="tsqr", block_rows=4096)
+    assert e.value.code == P.PQR_EPLAN
+    torch.cuda.synchronize()
+    # the largest supported leaf (1536 rows) works
+    X = dev(inputs.gaussian(6, n, 8))
+    with P.PQR(n, 16, 8, Q, variant="tsqr", block_rows=1536) as h:
+        assert h.solve(X, U=empty(n, 8), flags=P.PQR_NO_APPEND) == 8
+        assert 1024 < h.stats()["block_rows"] <= 1536  # blocks are spread evenly over the rows
