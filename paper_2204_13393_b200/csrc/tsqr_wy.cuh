@@ -169,20 +169,20 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   };
   // fixed-order sum of the kWyWarps partials: G = kWyThreads / E threads per entry;
   // partials are entry-major with stride kWyWarps + 1 (conflict-free for writers and readers)
-  const int rz_G = kWyThreads / E;  // threads per entry (8 or 2)
-  const int rz_e = tid / rz_G, rz_part = tid - rz_e * rz_G;
+  // 2 threads per entry (the first 2E threads): 8 partials each, one xor step
+  const int rz_e = tid >> 1, rz_part = tid & 1;
   const double* rz_src = red + rz_e * (kWyWarps + 1) + rz_part;
   auto reduce_Z = [&]() {
-    double z = rz_src[0];
-    for (int ww = rz_G; ww < kWyWarps; ww += rz_G) z += rz_src[ww];
-    if (rz_G == 8) {
+    if (tid < 2 * E) {
+      double z0 = rz_src[0], z1 = rz_src[2], z2 = rz_src[4], z3 = rz_src[6];
+      z0 += rz_src[8];
+      z1 += rz_src[10];
+      z2 += rz_src[12];
+      z3 += rz_src[14];
+      double z = (z0 + z1) + (z2 + z3);
       z += __shfl_xor_sync(0xffffffffu, z, 1);
-      z += __shfl_xor_sync(0xffffffffu, z, 2);
-      z += __shfl_xor_sync(0xffffffffu, z, 4);
-    } else {
-      z += __shfl_xor_sync(0xffffffffu, z, 1);
+      if (rz_part == 0) Zs[rz_e] = z;
     }
-    if (rz_part == 0) Zs[rz_e] = z;
   };
   // optional phase tracing (CTA 0, warps 0 and 15, lane 0): cycles per phase in smem.
   // Compiled in only with -DPQR_WY_TRACE (tools: build.py --trace); absent from the product build.
