@@ -30,8 +30,9 @@ def deps():
     return sorted(glob.glob(os.path.join(CSRC, "*")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    """trace=True compiles the TSQR phase counters in (PQR_WY_TRACE=1 then prints them)."""
+def build(force: bool = False, verbose: bool = False, trace: bool = False, defines=()) -> str:
+    """trace=True compiles the TSQR phase counters in (PQR_WY_TRACE=1 then prints them);
+    defines: extra -D flags (tuning builds, e.g. -DPQR_WY_WARPS=8)."""
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps()):
@@ -40,7 +41,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3",
-           "-I", inc, "-I", os.path.join(ROOT, "include"), *(["-DPQR_WY_TRACE"] if trace else []),
+           "-I", inc, "-I", os.path.join(ROOT, "include"), *(["-DPQR_WY_TRACE"] if trace else []), *defines,
            *sources(), "-o", tmp,
            "-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}", "-lcudart"]
     subprocess.check_call(cmd)
@@ -49,4 +50,5 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv,
+                defines=[a for a in sys.argv[1:] if a.startswith("-D")]))

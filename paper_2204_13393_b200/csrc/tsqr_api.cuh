@@ -75,7 +75,7 @@ cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int 
                       cudaStream_t st) {
   auto f = k_wy_down<UW, NT, WM>;
   ensure_smem(f, smem);
-  f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
+  f<<<grid, 32 * kWyDownWarps + 128, smem, st>>>(L, P, Call, t, ncol);
   return cudaGetLastError();
 }
 

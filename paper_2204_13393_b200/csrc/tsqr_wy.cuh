@@ -3,8 +3,9 @@
 // fp64 MMAs (mma.sync m8n8k4 .f64, SASS DMMA).
 //
 // Blocks of a level (leaf row blocks, or tree nodes) are processed by a persistent grid
-// (one 512-thread CTA per SM, CTA i takes blocks i, i + grid, ...).  A block holds
-// R <= 256*UW rows; warp w (of 16) owns UW units of 16 rows, lane (g = l>>2, q = l&3)
+// (one CTA per SM: NW = 16 consumer warps in stage 1, 8 in stage 2, plus a producer
+// warpgroup; CTA i takes blocks i, i + grid, ...).  A block holds R <= 16*NW*UW rows;
+// consumer warp w owns UW units of 16 rows, lane (g = l>>2, q = l&3)
 // keeping rows 16u+4q+{0..3} of columns 8nt+g in registers (the D-fragment layout of the
 // update MMA below).  The block's reflectors are grouped in panels (the s reflectors one
 // call creates, or one LOR-build chunk): H_a ... H_b = I - V T V^T with
@@ -36,11 +37,21 @@
 
 namespace pqr {
 
-constexpr int kWyWarps = 16;
-constexpr int kWyThreads = 32 * kWyWarps;       // consumer threads
+// Consumer warps: 16 in stage 1 (its Householder tail wants many lanes), 8 in stage 2 (measured
+// faster: cheaper barriers and partial sums, twice the rows and independent MMAs per warp).
+// UW below is per-warp units for the kernel's own warp count; the host plans in 16-warp units.
+#ifndef PQR_WY_DOWN_WARPS
+#define PQR_WY_DOWN_WARPS 8
+#endif
+constexpr int kWyWarps = 16;                     // stage-1 consumer warps (and the smem layout's maximum)
+constexpr int kWyDownWarps = PQR_WY_DOWN_WARPS;  // stage-2 consumer warps
+static_assert(kWyDownWarps == 8 || kWyDownWarps == 16, "stage-2 consumer warps");
+constexpr int kWyDownScale = kWyWarps / kWyDownWarps;  // stage-2 UW = host UW x this
+constexpr int kWyThreads = 32 * kWyWarps;        // stage-1 consumer threads
 constexpr int kWyLaunch = kWyThreads + 128;      // + one producer warpgroup (one working lane)
-constexpr int kWyConsumerRegs = 112;  // setmaxnreg split of the launch allocation (640 x 96):
-                                      // 4 x 128 x 112 + 128 x 24 <= 640 x 96
+constexpr int kWyConsumerRegs = 112;  // setmaxnreg split of the 16-warp launch allocation
+                                      // (640 x 96): 4 x 128 x 112 + 128 x 24 <= 640 x 96; the
+                                      // 8-warp launch (384 x 168) needs no split
 constexpr int kWyProducerRegs = 24;
 constexpr int kWyRowsPerUW = 16 * kWyWarps;  // block rows covered per unit-per-warp
 constexpr int kWyMaxW = 16;                  // widest panel
@@ -83,9 +94,11 @@ inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
          (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t);
 }
 
-template <int UW, int NT, int WM, bool UP, bool MERGE = false>
+template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false>
 PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge_,
                      int mtoff) {
+  constexpr int NTH = 32 * NW, NLA = NTH + 128;  // consumer threads, launch size
+  static_assert(NW == 8 || NW == 16, "consumer warps");
   constexpr bool merge = MERGE;  // separate instantiation: the common path carries no merge code
   (void)merge_;
   extern __shared__ __align__(16) double sm[];
@@ -94,9 +107,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
   const int E = wm * wm;
   double* ring = sm;
-  double* red = ring + (size_t)nbuf * SS;  // E x (kWyWarps + 1): per-warp partials, entry-major (padded)
+  double* red = ring + (size_t)nbuf * SS;  // E x (NW + 1): per-warp partials, entry-major (padded)
   double* Zs = red + (kWyWarps + 1) * E;   // E: reduced Z (ld wm)
-  double* hred = Zs + E;                   // 2 x (kWyWarps*16 partials + 16 pivot-row values)
+  double* hred = Zs + E;                   // 2 x (NW*16 partials + 16 pivot-row values)
   double* diagv = hred + kWyHH;            // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
   double* hfc = tsc + 512;                 // 2 x 32: Householder-round coefficients (by round parity)
@@ -113,12 +126,12 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   const int64_t total = (int64_t)nb_cta * ipb;
 
   // never-copied slot parts must hold finite values (they meet zero coefficients)
-  for (int e = tid; e < nbuf * SS; e += kWyLaunch) ring[e] = 0.0;
-  for (int i = tid; i < np; i += kWyLaunch) pans[i] = P.pan[i];
+  for (int e = tid; e < nbuf * SS; e += NLA) ring[e] = 0.0;
+  for (int i = tid; i < np; i += NLA) pans[i] = P.pan[i];
   if (tid == 0) {
     for (int i = 0; i < nbuf; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kWyWarps);
+      mbar_init(&empty[i], NW);
     }
     fence_mbar_init();
   }
@@ -127,9 +140,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 
   // ---- producer warp: streams ring item `it` into slot it % nbuf once the consumers have
   // released the slot's previous item (empty barrier, one arrival per consumer warp) ----
-  if (warp >= kWyWarps) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWyProducerRegs));
-    if (warp == kWyWarps && lane == 0) {
+  if (warp >= NW) {
+    if constexpr (NW == 16) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWyProducerRegs));
+    if (warp == NW && lane == 0) {
       for (int it = 0; it < total; ++it) {
         const int jb = it / ipb;
         const int p = it - jb * ipb;
@@ -159,36 +172,45 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     }
     return;
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kWyConsumerRegs));
-  // consumer warps only from here: named barrier 1 over the kWyThreads consumer threads
-  auto cbar = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(kWyThreads) : "memory"); };
+  if constexpr (NW == 16) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kWyConsumerRegs));
+  // consumer warps only from here: named barrier 1 over the NTH consumer threads
+  auto cbar = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory"); };
   // this warp is done with ring item `it` (all of its lanes' reads precede the arrival)
   auto release = [&](int64_t it) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[it % nbuf]);
   };
-  // fixed-order sum of the kWyWarps partials: G = kWyThreads / E threads per entry;
-  // partials are entry-major with stride kWyWarps + 1 (conflict-free for writers and readers)
-  // 2 threads per entry (the first 2E threads): 8 partials each, one xor step
-  const int rz_e = tid >> 1, rz_part = tid & 1;
-  const double* rz_src = red + rz_e * (kWyWarps + 1) + rz_part;
+  // fixed-order sum of the NW partials;
+  // partials are entry-major with stride NW + 1 (conflict-free for writers and readers)
+  // 16 warps: 2 threads per entry (the first 2E threads), 8 partials each, one xor step;
+  // 8 warps: one thread per entry (E <= NTH), 8 partials
+  const int rz_e = NW == 16 ? tid >> 1 : tid, rz_part = NW == 16 ? tid & 1 : 0;
+  const double* rz_src = red + rz_e * (NW + 1) + rz_part;
   auto reduce_Z = [&]() {
-    if (tid < 2 * E) {
-      double z0 = rz_src[0], z1 = rz_src[2], z2 = rz_src[4], z3 = rz_src[6];
-      z0 += rz_src[8];
-      z1 += rz_src[10];
-      z2 += rz_src[12];
-      z3 += rz_src[14];
-      double z = (z0 + z1) + (z2 + z3);
-      z += __shfl_xor_sync(0xffffffffu, z, 1);
-      if (rz_part == 0) Zs[rz_e] = z;
+    if constexpr (NW == 16) {
+      if (tid < 2 * E) {
+        double z0 = rz_src[0], z1 = rz_src[2], z2 = rz_src[4], z3 = rz_src[6];
+        z0 += rz_src[8];
+        z1 += rz_src[10];
+        z2 += rz_src[12];
+        z3 += rz_src[14];
+        double z = (z0 + z1) + (z2 + z3);
+        z += __shfl_xor_sync(0xffffffffu, z, 1);
+        if (rz_part == 0) Zs[rz_e] = z;
+      }
+    } else {
+      if (tid < E) {
+        const double z0 = rz_src[0] + rz_src[4], z1 = rz_src[1] + rz_src[5];
+        const double z2 = rz_src[2] + rz_src[6], z3 = rz_src[3] + rz_src[7];
+        Zs[rz_e] = (z0 + z2) + (z1 + z3);
+      }
     }
   };
   // optional phase tracing (CTA 0, warps 0 and 15, lane 0): cycles per phase in smem.
   // Compiled in only with -DPQR_WY_TRACE (tools: build.py --trace); absent from the product build.
 #ifdef PQR_WY_TRACE
   __shared__ unsigned long long s_tr[2][16];
-  const bool tr_on = L.trace != nullptr && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == kWyWarps - 1);
+  const bool tr_on = L.trace != nullptr && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == NW - 1);
   const int tr_w = warp == 0 ? 0 : 1;
   long long tr_t0 = 0;
   if (tr_on) {
@@ -211,7 +233,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     const int64_t b = blockIdx.x + (int64_t)jb * gridDim.x;
     const int64_t r0 = wy_start(L, b);
     const int R = wy_rows(L, b);
-    const bool mrow = kWyRowsPerUW / kWyWarps * UW * (warp + 1) > R;  // warp holds rows >= R
+    const bool mrow = 16 * UW * (warp + 1) > R;  // warp holds rows >= R
     double x[UW][NT][4];
     if (UP) {
       WY_TR(9);
@@ -296,8 +318,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             dmma884(d0, d1, (q & 1) ? s1 : s0, bt);
           }
           // D[c = 8nt+g][j = 2q + v] of this warp's partial of Z'^T
-          red[((2 * q) + wm * (8 * nt + g)) * (kWyWarps + 1) + warp] = d0;
-          red[((2 * q + 1) + wm * (8 * nt + g)) * (kWyWarps + 1) + warp] = d1;
+          red[((2 * q) + wm * (8 * nt + g)) * (NW + 1) + warp] = d0;
+          red[((2 * q + 1) + wm * (8 * nt + g)) * (NW + 1) + warp] = d1;
         }
         WY_TR(1);
         cbar();  // B1: partials complete; every warp is done with the previous item
@@ -344,7 +366,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int v = 0; v < 2; ++v)
-              red[((8 * mt + g) + wm * (8 * nt + 2 * q + v)) * (kWyWarps + 1) + warp] = acc[0][mt][nt][v] + acc[1][mt][nt][v];
+              red[((8 * mt + g) + wm * (8 * nt + 2 * q + v)) * (NW + 1) + warp] = acc[0][mt][nt][v] + acc[1][mt][nt][v];
         }
       }
       WY_TR(1);
@@ -531,14 +553,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
       if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
       const int vi = (lane / LG) & (S8 - 1);
-      double* hb = hred + hpar * (kWyWarps * kWyHS + 16);
+      double* hb = hred + hpar * (NW * kWyHS + 16);
       hpar ^= 1;
       if ((lane & (LG - 1)) == 0) hb[warp * kWyHS + vi] = D[0];
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
         if (rowk[e] == r) {
 #pragma unroll
-          for (int cc = 0; cc < S8; ++cc) hb[kWyWarps * kWyHS + cc] = xr[e][cc];
+          for (int cc = 0; cc < S8; ++cc) hb[NW * kWyHS + cc] = xr[e][cc];
         }
       WY_TR(11);
       cbar();
@@ -548,7 +570,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       // (cheaper than every warp reducing and broadcasting the totals itself).
       double* hf = hfc + (c & 1) * 32;  // [0, S8): coefficients; S8: inv; S8+1: u0 - sigma*lambda
       if (warp == 0) {
-        constexpr int NP = 32 / S8, WPP = kWyWarps / NP;  // lane groups, warps per group
+        constexpr int NP = 32 / S8, WPP = NW / NP;  // lane groups, warps per group
         const int v = lane & (S8 - 1), part = lane / S8;
         const double* hv = hb + part * WPP * kWyHS + v;
         double tot = 0.0;
@@ -557,14 +579,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
         for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
         const double lam2 = __shfl_sync(0xffffffffu, tot, c);
-        const double u0 = hb[kWyWarps * kWyHS + c];
+        const double u0 = hb[NW * kWyHS + c];
         const double lam = sqrt(lam2);
         const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
         const double diag = sigma * lam;
         const double nv2 = 2.0 * lam * (lam + fabs(u0));
         const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
         // v . x_v (v > c: update coefficient / 2) and v_v . v_c (v < c: column c of V^T V)
-        const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[kWyWarps * kWyHS + v]);
+        const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[NW * kWyHS + v]);
         if (lane < S8) {
           hf[lane] = fv;
           if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
@@ -641,16 +663,16 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         }
       }
       Dp[0] += __shfl_xor_sync(0xffffffffu, Dp[0], 1);
-      double* hb = hred + hpar * (kWyWarps * kWyHS + 16);
+      double* hb = hred + hpar * (NW * kWyHS + 16);
       hpar ^= 1;
       if ((lane & 1) == 0) hb[warp * kWyHS + ((lane >> 1) & 15)] = Dp[0];
       cbar();
       if (warp == 0) {
-        // C = V1^T V2 (w1 x s, entry j*s + c): lane l sums value l & 15 over 8 warps, xor 16
+        // C = V1^T V2 (w1 x s, entry j*s + c): lane l sums value l & 15 over half the warps, xor 16
         const int v = lane & 15, part = lane >> 4;
         double tot = 0.0;
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) tot += hb[(part * 8 + ww) * kWyHS + v];
+        for (int ww = 0; ww < NW / 2; ++ww) tot += hb[(part * (NW / 2) + ww) * kWyHS + v];
         tot += __shfl_xor_sync(0xffffffffu, tot, 16);
         double* Cm = tsc + 256 + 16 * 8;  // 16 scratch words after the T columns (s <= 8 here)
         if (lane < 16) Cm[lane] = tot;
@@ -708,13 +730,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 
 template <int UW, int NT, int WM, bool MERGE>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<UW, NT, WM, true, MERGE>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<kWyWarps, UW, NT, WM, true, MERGE>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
+// (UW in 16-warp units, as planned by the host)
 template <int UW, int NT, int WM>
-__global__ void __launch_bounds__(kWyLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  wy_body<UW, NT, WM, false>(L, P, 0, t, Call, ncol, 0, 0);
+__global__ void __launch_bounds__(32 * kWyDownWarps + 128, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
+  wy_body<kWyDownWarps, UW * kWyDownScale, NT, WM, false>(L, P, 0, t, Call, ncol, 0, 0);
 }
 
 }  // namespace pqr
