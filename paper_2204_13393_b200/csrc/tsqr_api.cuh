@@ -122,6 +122,7 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   TsqrState* ts = h->ts;
   WyLevel L = to_wy(ts, lv);
   L.X = X; L.ldx = ldx; L.out = out; L.ldo = ldo;
+  L.ovec = ((ts->cap & 1) == 0 && (ldo & 1) == 0 && aligned16(out)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);

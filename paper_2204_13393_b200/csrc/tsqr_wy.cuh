@@ -67,6 +67,7 @@ struct WyLevel {
                                     // and row R of an odd-sized last block is a zero pad row
   double* T; int64_t tstride;       // block b's T area at T + b*tstride; panel at +16*start
   double* out; int64_t ldo;         // stage-1 output: block b -> rows b*cap ...
+  int ovec;                         // out 16-B aligned with even cap and ldo (paired stores)
   const double* cin; int64_t ldci;  // stage-2 coefficients: block b -> rows b*cap ...
   double* Y; int64_t ldy;           // stage-2 output (level rows)
   int yvec;                         // Y 16-B aligned with even ldy (paired stores)
@@ -702,6 +703,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     }
     WY_TR(8);
     // ---------------- outputs: [P_b; N_b] to the parent slot, the new reflectors ----------------
+    // With RPL even a lane's rows come in consecutive pairs (rowk[e + 1] = rowk[e] + 1 for even e),
+    // so a warp writes each column as one contiguous 16-byte-per-lane store.
     {
       double* outb = L.out + b * L.cap;
       const int rmax = R < L.cap ? R : L.cap;
@@ -710,11 +713,33 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         if (c >= s) break;
         const int piv = C + c;
         const double dg = diagv[c];
+        double* vcol = L.V + r0 + (int64_t)(C + c) * L.ldv;
+        double* ocol = outb + (int64_t)c * L.ldo;
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
           const int row = rowk[e];
-          if (row < rmax) outb[row + (int64_t)c * L.ldo] = row < piv ? xr[e][c] : (row == piv ? dg : 0.0);
-          if (row < R) L.V[r0 + row + (int64_t)(C + c) * L.ldv] = row >= piv ? xr[e][c] : 0.0;
+          const double ov = row < piv ? xr[e][c] : (row == piv ? dg : 0.0);
+          const double vv = row >= piv ? xr[e][c] : 0.0;
+          if constexpr (RPL % 2 == 0) {
+            if (e % 2 == 0) {
+              const double ov1 = row + 1 < piv ? xr[e + 1][c] : (row + 1 == piv ? dg : 0.0);
+              const double vv1 = row + 1 >= piv ? xr[e + 1][c] : 0.0;
+              if (row + 1 < R) {
+                st2(vcol + row, vv, vv1);
+              } else if (row < R) {
+                vcol[row] = vv;
+              }
+              if (L.ovec && row + 1 < rmax) {
+                st2(ocol + row, ov, ov1);
+              } else {
+                if (row < rmax) ocol[row] = ov;
+                if (row + 1 < rmax) ocol[row + 1] = ov1;
+              }
+            }
+          } else {
+            if (row < rmax) ocol[row] = ov;
+            if (row < R) vcol[row] = vv;
+          }
         }
       }
     }
