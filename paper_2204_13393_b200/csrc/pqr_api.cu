@@ -56,6 +56,18 @@ void tsqr_free(Ctx* h);
 
 struct TsqrState;  // defined in tsqr_api.cuh
 
+// Host-buffer pipeline (pqr_project_normalize with host X and U, one rank): X goes up and U
+// comes back in row chunks on a second stream, each chunk's copy overlapped with the kernels
+// of the other chunks (the first and the last pass are launched per chunk).
+constexpr int kHostChunksMax = 16;
+struct HostPipe {
+  int nch = 0;                          // chunks of this call (0: not pipelined)
+  int64_t r[kHostChunksMax + 1] = {};   // row boundaries
+  int64_t b[kHostChunksMax + 1] = {};   // TSQR leaf-block boundaries (rows r[c] = start of block b[c])
+  const double* Xh = nullptr; int64_t ldxh = 0;
+  double* Uh = nullptr; int64_t lduh = 0;
+};
+
 struct Ctx {
   pqr_config cfg{};
   cudaStream_t stream = nullptr;
@@ -77,6 +89,10 @@ struct Ctx {
   double* stageX = nullptr;  // n x s_max staging for host X
   double* stageU = nullptr;  // n x s_max staging for host U / internal U1
   double* stageC = nullptr;  // cap x 16 staging for host C
+  HostPipe hp;
+  cudaStream_t cstream = nullptr;  // copy stream of the host-buffer pipeline (created on first use)
+  cudaEvent_t hp_in[kHostChunksMax] = {}, hp_out[kHostChunksMax] = {}, hp_done = nullptr;
+  double* Wchunks = nullptr;       // kHostChunksMax x (cap x s_max): per-chunk Grams of the first pass
   ncclComm_t comm = nullptr;
   pqr_stats st{};
   TsqrState* ts = nullptr;
@@ -152,6 +168,77 @@ int dalloc(T** p, size_t count) {
   if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) {
     cudaGetLastError();
     return PQR_ENOMEM;
+  }
+  return PQR_OK;
+}
+
+// ---- host-buffer pipeline helpers (HostPipe) ----
+int hp_wait_in(Ctx* h, int c) {
+  CUDA_TRY(cudaStreamWaitEvent(h->stream, h->hp_in[c], 0));
+  return PQR_OK;
+}
+// U rows of chunk c (device Ud, ld ldud; ncol columns) to the caller's host U once the stream
+// has produced them
+int hp_d2h_chunk(Ctx* h, int c, const double* Ud, int64_t ldud, int ncol) {
+  HostPipe& p = h->hp;
+  CUDA_TRY(cudaEventRecord(h->hp_out[c], h->stream));
+  CUDA_TRY(cudaStreamWaitEvent(h->cstream, h->hp_out[c], 0));
+  const int64_t r0 = p.r[c], rows = p.r[c + 1] - p.r[c];
+  if (rows > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(p.Uh + r0, p.lduh * sizeof(double), Ud + r0, ldud * sizeof(double),
+                               rows * sizeof(double), ncol, cudaMemcpyDeviceToHost, h->cstream));
+  return PQR_OK;
+}
+// the call's stream waits for the copy stream (the caller's one synchronisation covers both)
+int hp_finish(Ctx* h) {
+  if (h->hp.nch == 0) return PQR_OK;
+  CUDA_TRY(cudaEventRecord(h->hp_done, h->cstream));
+  CUDA_TRY(cudaStreamWaitEvent(h->stream, h->hp_done, 0));
+  return PQR_OK;
+}
+// Decide the chunking and enqueue the chunked X upload into stageX.  Chunk count: PQR_HOST_CHUNKS
+// (default 8 from 2^18 rows; 0 or 1 disables), rows per chunk a multiple of 64 (CholQR2) or whole leaf
+// blocks (TSQR, `bounds` = leaf-block start rows, nb + 1 entries).
+int hp_plan_upload(Ctx* h, const double* X, int64_t ldx, int s, double* U, int64_t ldu,
+                   const std::vector<int64_t>* bounds) {
+  HostPipe& p = h->hp;
+  p.nch = 0;
+  const char* env = getenv("PQR_HOST_CHUNKS");  // read per call (tests switch it)
+  const int want = std::min(env ? atoi(env) : 8, kHostChunksMax);
+  const int64_t n = h->cfg.n_local;
+  // by default only problems large enough for the copies to dominate (>= 2^18 rows)
+  if (want < 2 || n < (env ? (int64_t)64 * want : (int64_t)1 << 18)) return PQR_OK;
+  if (!h->cstream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    for (int c = 0; c < kHostChunksMax; ++c) {
+      CUDA_TRY(cudaEventCreateWithFlags(&h->hp_in[c], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&h->hp_out[c], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&h->hp_done, cudaEventDisableTiming));
+  }
+  int nch = want;
+  if (bounds) {
+    const int64_t nb = (int64_t)bounds->size() - 1;
+    nch = (int)std::min<int64_t>(nch, nb);
+    for (int c = 0; c <= nch; ++c) {
+      p.b[c] = nb * c / nch;
+      p.r[c] = (*bounds)[p.b[c]];
+    }
+  } else {
+    const int64_t step = ((n + nch - 1) / nch + 63) / 64 * 64;
+    for (int c = 0; c <= nch; ++c) p.r[c] = std::min<int64_t>(n, (int64_t)c * step);
+  }
+  p.nch = nch;
+  p.Xh = X; p.ldxh = ldx; p.Uh = U; p.lduh = ldu;
+  // the copy stream may only overwrite stageX once earlier work on the call's stream is done
+  CUDA_TRY(cudaEventRecord(h->hp_done, h->stream));
+  CUDA_TRY(cudaStreamWaitEvent(h->cstream, h->hp_done, 0));
+  for (int c = 0; c < nch; ++c) {
+    const int64_t r0 = p.r[c], rows = p.r[c + 1] - p.r[c];
+    if (rows > 0)
+      CUDA_TRY(cudaMemcpy2DAsync(h->stageX + r0, h->ld * sizeof(double), X + r0, ldx * sizeof(double),
+                                 rows * sizeof(double), s, cudaMemcpyHostToDevice, h->cstream));
+    CUDA_TRY(cudaEventRecord(h->hp_in[c], h->cstream));
   }
   return PQR_OK;
 }
@@ -442,7 +529,20 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
   // pass 1: W1 = [Q X]^T X -> P1, N1, M1, t1 -> U1 = [Q X] M1
   const double* Wsum = nullptr;
   int nparts = 1;
-  TRY(gram_and_exchange(h, k, s, h->basis, X, ldx, &Wsum, &nparts));
+  if (h->hp.nch > 0) {
+    // host X: one Gram per uploaded chunk; k_factor sums the chunk Grams in chunk order
+    PROF(h, PQR_K_GRAM);
+    for (int c = 0; c < h->hp.nch; ++c) {
+      const int64_t r0 = h->hp.r[c];
+      TRY(hp_wait_in(h, c));
+      TRY(run_gram(h->hp.r[c + 1] - r0, k, s, h->basis + r0, h->ld, X + r0, ldx, h->Wchunks + (size_t)c * m * s, m,
+                   h->partials, h->ticket, h->sms, h->stream, &h->st.kernel_launches));
+    }
+    Wsum = h->Wchunks;
+    nparts = h->hp.nch;
+  } else {
+    TRY(gram_and_exchange(h, k, s, h->basis, X, ldx, &Wsum, &nparts));
+  }
   FactorArgs f{};
   f.W = Wsum; f.w_stride = (int64_t)m * s; f.nparts = nparts; f.ldw = m; f.k = k; f.s = s; f.s_dev = nullptr;
   f.tol2 = tol2; f.eta = eta;
@@ -487,7 +587,16 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
       PROF(h, PQR_K_FACTOR);
       TRY(run_factor(f2, h->stream, &h->st.kernel_launches));
     }
-    {
+    if (h->hp.nch > 0) {
+      // host U: the final pass per chunk, each chunk's rows copied out behind it
+      PROF(h, PQR_K_UPDATE);
+      for (int c = 0; c < h->hp.nch; ++c) {
+        const int64_t r0 = h->hp.r[c];
+        TRY(run_update(h->hp.r[c + 1] - r0, k, h->basis + r0, h->ld, s, Ud + r0, ldud, h->M2, m, s, d_t2, Ud + r0,
+                       ldud, Uappend ? Uappend + r0 : nullptr, h->ld, h->sms, h->stream, &h->st.kernel_launches));
+        TRY(hp_d2h_chunk(h, c, Ud, ldud, s));
+      }
+    } else {
       PROF(h, PQR_K_UPDATE);
       TRY(run_update(n, k, h->basis, h->ld, s, Ud, ldud, h->M2, m, s, d_t2, Ud, ldud, Uappend, h->ld, h->sms,
                      h->stream, &h->st.kernel_launches));
@@ -650,17 +759,30 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   const bool append = !(flags & PQR_NO_APPEND);
   if (!append && !U) return PQR_EARG;
 
-  // stage host inputs
+  // stage host inputs (host X and U on one rank: pipelined in row chunks, HostPipe)
   const double* Xd = X;
   int64_t ldxd = ldx;
-  if (is_host_ptr(X)) {
+  const bool x_host = is_host_ptr(X);
+  const bool u_host = U && is_host_ptr(U);
+  h->hp.nch = 0;
+  if (x_host) {
     if (!h->stageX && dalloc(&h->stageX, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
-    CUDA_TRY(cudaMemcpy2DAsync(h->stageX, h->ld * sizeof(double), X, ldx * sizeof(double), n * sizeof(double), s,
-                               cudaMemcpyHostToDevice, h->stream));
+    if (u_host && !h->comm && !(flags & PQR_SINGLE_PASS)) {
+      if (h->cfg.variant == PQR_CHOLQR2) {
+        if (!h->Wchunks && dalloc(&h->Wchunks, (size_t)kHostChunksMax * h->cap * h->cfg.s_max)) return PQR_ENOMEM;
+        TRY(hp_plan_upload(h, X, ldx, s, U, ldu, nullptr));
+      } else {
+        std::vector<int64_t> bounds;
+        tsqr_leaf_bounds(h, &bounds);
+        TRY(hp_plan_upload(h, X, ldx, s, U, ldu, &bounds));
+      }
+    }
+    if (h->hp.nch == 0)
+      CUDA_TRY(cudaMemcpy2DAsync(h->stageX, h->ld * sizeof(double), X, ldx * sizeof(double), n * sizeof(double), s,
+                                 cudaMemcpyHostToDevice, h->stream));
     Xd = h->stageX;
     ldxd = h->ld;
   }
-  const bool u_host = U && is_host_ptr(U);
   double* Ud = nullptr;
   int64_t ldud = 0;
   if (U && !u_host && (ldu & 1) == 0 && aligned16(U)) {
@@ -683,9 +805,14 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   } else {
     rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
   }
-  if (rc != PQR_OK) return rc;
+  if (rc != PQR_OK) {
+    if (h->hp.nch > 0) cudaStreamSynchronize(h->cstream);
+    h->hp.nch = 0;
+    return rc;
+  }
   // outputs (enqueued before the one synchronisation of the call)
-  if (U && Ud != U) {
+  TRY(hp_finish(h));
+  if (U && Ud != U && h->hp.nch == 0) {
     CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, ldud * sizeof(double), n * sizeof(double), s,
                                cudaMemcpyDefault, h->stream));
   }
@@ -696,6 +823,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
     CUDA_TRY(cudaMemcpy2DAsync(N, (size_t)ldn * sizeof(double), h->Nf, (size_t)kSMax * sizeof(double),
                                (size_t)s * sizeof(double), s, cudaMemcpyDefault, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->hp.nch = 0;
   prof_collect(h);
   tt = h->h_ints[2];
   if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;  // basis unchanged
@@ -760,7 +888,16 @@ int pqr_destroy(pqr_handle hh) {
   cudaFree(h->Pf); cudaFree(h->Nf);
   cudaFree(h->ints);
   if (h->h_ints) cudaFreeHost(h->h_ints);
-  cudaFree(h->stageX); cudaFree(h->stageU); cudaFree(h->stageC);
+  cudaFree(h->stageX); cudaFree(h->stageU); cudaFree(h->stageC); cudaFree(h->Wchunks);
+  if (h->cstream) {
+    cudaStreamSynchronize(h->cstream);
+    for (int c = 0; c < kHostChunksMax; ++c) {
+      cudaEventDestroy(h->hp_in[c]);
+      cudaEventDestroy(h->hp_out[c]);
+    }
+    cudaEventDestroy(h->hp_done);
+    cudaStreamDestroy(h->cstream);
+  }
   if (h->comm) ncclCommDestroy(h->comm);
   for (auto& p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
   for (auto e : h->ev_pool) cudaEventDestroy(e);

@@ -111,6 +111,7 @@ void wy_trace_dump(const char* kind, const WyLevel& L, cudaStream_t st) {
 WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
   WyLevel L{};
   L.q = lv.q; L.rem2 = lv.rem2; L.odd_last = lv.odd_last; L.nblocks = lv.nblocks;
+  L.b0 = 0; L.nrun = lv.nblocks;
   L.V = lv.V; L.ldv = lv.ldv; L.T = lv.T; L.tstride = lv.tstride;
   L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax; L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap);
   L.trace = wy_trace_buf();
@@ -118,15 +119,17 @@ WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
 }
 
 int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* out, int64_t ldo, int np, int C,
-              int s, int merge = 0, int mtoff = 0) {
+              int s, int merge = 0, int mtoff = 0, int64_t b0 = 0, int64_t nrun = -1) {
   TsqrState* ts = h->ts;
   WyLevel L = to_wy(ts, lv);
+  if (nrun >= 0) { L.b0 = b0; L.nrun = nrun; }
+  if (L.nrun == 0) return PQR_OK;
   L.X = X; L.ldx = ldx; L.out = out; L.ldo = ldo;
   L.ovec = ((ts->cap & 1) == 0 && (ldo & 1) == 0 && aligned16(out)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
-  const int grid = std::min(lv.nblocks, h->sms);
+  const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
 #define UPC(U, N, W) wy_up_t<U, N, W>(L, P, C, s, merge, mtoff, grid, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, ts->wmax, UPC)
@@ -141,15 +144,17 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
 }
 
 int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, double* Y, int64_t ldy, int np,
-                int Call, int t, int ncol, const int4* pan) {
+                int Call, int t, int ncol, const int4* pan, int64_t b0 = 0, int64_t nrun = -1) {
   TsqrState* ts = h->ts;
   WyLevel L = to_wy(ts, lv);
+  if (nrun >= 0) { L.b0 = b0; L.nrun = nrun; }
+  if (L.nrun == 0) return PQR_OK;
   L.cin = cin; L.ldci = ldci; L.Y = Y; L.ldy = ldy;
   L.yvec = ((ldy & 1) == 0 && aligned16(Y)) ? 1 : 0;
   WyPanels P{pan, np};
   const int NT = ncol > 8 ? 2 : 1;
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
-  const int grid = std::min(lv.nblocks, h->sms);
+  const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
 #define DNC(U, N, W) wy_down_t<U, N, W>(L, P, Call, t, ncol, grid, smem, h->stream)
   PQR_WY_SWITCH(lv.UW, NT, ts->wmax, DNC)
@@ -165,14 +170,23 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
 
 // Stage 1 over all levels: X (n_local x s) -> Btop ((C+s) x s, ld cap).  Creates s new
 // reflectors (one new panel) at every level.
-int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, int mtoff = 0) {
+int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, int mtoff = 0, bool pipe = false) {
   TsqrState* ts = h->ts;
   const int C = ts->C;
   const int np = (int)ts->panels.size();
   {
     PROF(h, PQR_K_TSQR_LOCAL);
-    TRY(run_wy_up(h, ts->lv[0], X, ldx, ts->nlev >= 1 ? ts->lv[1].in : ts->in_top,
-                  ts->nlev >= 1 ? ts->lv[1].rows : ts->cap, np, C, s, merge, mtoff));
+    double* out0 = ts->nlev >= 1 ? ts->lv[1].in : ts->in_top;
+    const int64_t ldo0 = ts->nlev >= 1 ? ts->lv[1].rows : ts->cap;
+    if (pipe && h->hp.nch > 0) {
+      // host X arrives chunk by chunk (leaf blocks are independent in stage 1)
+      for (int c = 0; c < h->hp.nch; ++c) {
+        TRY(hp_wait_in(h, c));
+        TRY(run_wy_up(h, ts->lv[0], X, ldx, out0, ldo0, np, C, s, merge, mtoff, h->hp.b[c], h->hp.b[c + 1] - h->hp.b[c]));
+      }
+    } else {
+      TRY(run_wy_up(h, ts->lv[0], X, ldx, out0, ldo0, np, C, s, merge, mtoff));
+    }
   }
   {
     PROF(h, PQR_K_TSQR_TREE);
@@ -203,7 +217,7 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
 // Stage 2 over all levels: top coefficients cin (Call x ncol, ld cap) -> Y (n_local x ncol),
 // applying the first np panels.
 int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol, double* Y, int64_t ldy,
-                    const int4* pan) {
+                    const int4* pan, bool pipe = false) {
   TsqrState* ts = h->ts;
   const double* root_cin = cin;
   int64_t root_ld = ts->cap;
@@ -221,8 +235,17 @@ int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol
     }
   }
   PROF(h, PQR_K_TSQR_APPLY);
-  TRY(run_wy_down(h, ts->lv[0], ts->nlev >= 1 ? ts->lv[1].dn : root_cin, ts->nlev >= 1 ? ts->lv[1].rows : root_ld,
-                  Y, ldy, np, Call, t, ncol, pan));
+  const double* cin0 = ts->nlev >= 1 ? ts->lv[1].dn : root_cin;
+  const int64_t ldc0 = ts->nlev >= 1 ? ts->lv[1].rows : root_ld;
+  if (pipe && h->hp.nch > 0) {
+    // U leaves for the host chunk by chunk, each copy behind its chunk's stage-2 launch
+    for (int c = 0; c < h->hp.nch; ++c) {
+      TRY(run_wy_down(h, ts->lv[0], cin0, ldc0, Y, ldy, np, Call, t, ncol, pan, h->hp.b[c], h->hp.b[c + 1] - h->hp.b[c]));
+      TRY(hp_d2h_chunk(h, c, Y, ldy, ncol));
+    }
+  } else {
+    TRY(run_wy_down(h, ts->lv[0], cin0, ldc0, Y, ldy, np, Call, t, ncol, pan));
+  }
   return PQR_OK;
 }
 
@@ -398,6 +421,14 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
   return PQR_OK;
 }
 
+// start rows of the leaf blocks (nblocks + 1 entries, the last = n_local): host-pipeline chunking
+void tsqr_leaf_bounds(Ctx* h, std::vector<int64_t>* out) {
+  const TsqrLv& lv = h->ts->lv[0];
+  out->resize((size_t)lv.nblocks + 1);
+  for (int64_t b = 0; b < lv.nblocks; ++b) (*out)[b] = b * lv.q + 2 * std::min<int64_t>(b, lv.rem2);
+  (*out)[lv.nblocks] = h->cfg.n_local;
+}
+
 int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, double* Ud, int64_t ldud, bool append,
                int* t_host) {
   TsqrState* ts = h->ts;
@@ -422,17 +453,17 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
       ts->mtoff = 16 * ts->cap + 16 * pv.x;
     }
   }
-  TRY(tsqr_up_sweep(h, X, ldx, s, ts->merge, ts->mtoff));
+  TRY(tsqr_up_sweep(h, X, ldx, s, ts->merge, ts->mtoff, true));
   TRY(run_top(h, s, false, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
   // U~ columns >= t are zero, so the down sweep writes zeros there.
   if (ts->merge) {
     std::vector<int4> lst(ts->panels);
     lst.back() = make_int4(lst.back().x, 8, ts->mtoff, 1);
     CUDA_TRY(cudaMemcpyAsync(ts->d_panm, lst.data(), sizeof(int4) * np, cudaMemcpyHostToDevice, h->stream));
-    TRY(tsqr_down_sweep(h, np, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_panm));
+    TRY(tsqr_down_sweep(h, np, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_panm, true));
   } else {
     TRY(tsqr_stage_panel(h, s));
-    TRY(tsqr_down_sweep(h, np + 1, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_pan));
+    TRY(tsqr_down_sweep(h, np + 1, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_pan, true));
   }
   // t reaches the host with the caller's single synchronisation; the caller commits the
   // panel (tsqr_commit) once t is known and the call has not failed

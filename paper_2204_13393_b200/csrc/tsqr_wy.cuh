@@ -62,6 +62,7 @@ struct WyLevel {
   int64_t q, rem2;      // block b: q + 2*(b < rem2) rows starting at b*q + 2*min(b, rem2) (even);
   int odd_last;         // ... the last block has one more row when the level's row count is odd
   int nblocks;
+  int64_t b0, nrun;     // this launch processes blocks b0 .. b0 + nrun - 1 (host-buffer pipeline chunks)
   const double* X; int64_t ldx;     // stage-1 input (level rows); 16-B aligned, ldx even
   double* V; int64_t ldv;           // reflectors (level rows); column j = reflector j; ldv even,
                                     // and row R of an odd-sized last block is a zero pad row
@@ -122,7 +123,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   const int g = lane >> 2, q = lane & 3;
   const int np = P.np;
   const int ipb = np + (UP ? 1 : 0);  // ring items per block (stage 1: X first)
-  const int64_t nbl = L.nblocks;
+  const int64_t nbl = L.nrun;
   const int nb_cta = (int64_t)blockIdx.x < nbl ? (int)((nbl - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int64_t total = (int64_t)nb_cta * ipb;
 
@@ -149,7 +150,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         const int p = it - jb * ipb;
         const int slot = it % nbuf;
         if (it >= nbuf) mbar_wait(&empty[slot], (uint32_t)((it / nbuf - 1) & 1));
-        const int64_t b = blockIdx.x + (int64_t)jb * gridDim.x;
+        const int64_t b = L.b0 + blockIdx.x + (int64_t)jb * gridDim.x;
         const int64_t r0 = wy_start(L, b);
         const int R = wy_rows(L, b);
         double* buf = ring + (size_t)slot * SS;
@@ -231,7 +232,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   int64_t it = 0;  // consumer item cursor
   int hpar = 0;    // Householder-round buffer parity
   for (int jb = 0; jb < nb_cta; ++jb) {
-    const int64_t b = blockIdx.x + (int64_t)jb * gridDim.x;
+    const int64_t b = L.b0 + blockIdx.x + (int64_t)jb * gridDim.x;
     const int64_t r0 = wy_start(L, b);
     const int R = wy_rows(L, b);
     const bool mrow = 16 * UW * (warp + 1) > R;  // warp holds rows >= R

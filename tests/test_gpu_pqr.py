@@ -179,6 +179,44 @@ def test_host_buffers(P, orc, variant):
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("chunks,n", [(None, 300_000), ("3", 6000), ("16", 20_011)])
+def test_host_pipeline(P, orc, variant, chunks, n, monkeypatch):
+    """Host X and U on one rank: the upload, the first and the last pass run in row chunks on
+    two streams (HostPipe; default 8 chunks from 2^18 rows, PQR_HOST_CHUNKS forces it for small,
+    ragged n).  Results: the oracle's within the parity tolerance, the device-buffer path's to
+    rounding (the chunked Gram sums in chunk order), and the appended basis the same."""
+    import torch
+
+    if chunks is not None:
+        monkeypatch.setenv("PQR_HOST_CHUNKS", chunks)
+    k, s = 24, 8
+    Q = inputs.orthonormal(171, n, k)
+    X1 = np.asfortranarray(inputs.gaussian(172, n, s) + Q @ inputs.gaussian(173, k, s))
+    X2 = inputs.gaussian(174, n, s)
+    ref = orc.householder_pqr(Q, X1)
+    outs = {}
+    for mode in ("host", "device"):
+        U = np.zeros((n, s), order="F") if mode == "host" else empty(n, s)
+        Pm = np.zeros((k, s), order="F") if mode == "host" else empty(k, s)
+        Nm = np.zeros((s, s), order="F") if mode == "host" else empty(s, s)
+        with P.PQR(n, k + 2 * s, s, dev(Q), k=k, variant=variant) as h:
+            conv = (lambda a: a) if mode == "host" else dev
+            t1 = h.solve(conv(X1), U=U, P=Pm, N=Nm)  # appends
+            U1, P1, N1 = (np.array(U), np.array(Pm), np.array(Nm)) if mode == "host" else (host(U), host(Pm), host(Nm))
+            Pm2 = np.zeros((k + s, s), order="F") if mode == "host" else empty(k + s, s)
+            t2 = h.solve(conv(X2), U=U, P=Pm2, N=Nm, flags=P.PQR_NO_APPEND)
+            U2 = np.array(U) if mode == "host" else host(U)
+            P2 = np.array(Pm2) if mode == "host" else host(Pm2)
+        torch.cuda.synchronize()
+        outs[mode] = dict(t=(t1, t2), U1=U1, P1=P1, N1=N1, U2=U2, P2=P2)
+    hst, dv = outs["host"], outs["device"]
+    assert hst["t"] == dv["t"] == (s, s)
+    assert rel(hst["P1"], ref["P"]) < 1e-10 and rel(hst["N1"], ref["N"]) < 1e-10 and rel(hst["U1"], ref["U"]) < 1e-10
+    for key in ("U1", "P1", "N1", "U2", "P2"):
+        assert rel(hst[key], dv[key]) < 1e-12, key
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 def test_no_deflation_flag_breakdown(P, variant):
     n, k, s = 4000, 8, 4
     Q = inputs.orthonormal(91, n, k)
