@@ -53,7 +53,8 @@ def check_vs_oracle(out, ref, tol=1e-10):
 @pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("n,k,s", [(10_000, 32, 4), (4097, 13, 3), (20_000, 0, 8), (65_536, 128, 8),
                                    (30_001, 96, 16), (12, 3, 2), (300_007, 64, 8),
-                                   (20_011, 144, 16), (50_000, 152, 8)])  # last two: k + s = kMMax
+                                   (20_011, 144, 16), (50_000, 152, 8),  # these two: k + s = kMMax
+                                   (7777, 5, 1), (1000, 0, 1), (2049, 40, 7)])
 def test_vs_oracle_random(P, orc, variant, n, k, s):
     Q = inputs.orthonormal(7 + n, n, k)
     X = inputs.gaussian(8 + n, n, s)
@@ -99,6 +100,14 @@ def test_special_cases(P, variant):
     # X inside span(Q): t = 0, P = C
     out = solve(P, m["Q"], np.asfortranarray(m["Q"] @ m["C"]), variant=variant)
     assert out["t"] == 0 and rel(out["P"], m["C"]) < 1e-13 and np.all(out["N"] == 0)
+    # X = 0: t = 0, P = 0, N = 0 (every column deflates; no division by a zero norm)
+    out = solve(P, m["Q"], np.zeros((n, s), order="F"), variant=variant)
+    assert out["t"] == 0 and np.all(out["P"] == 0) and np.all(out["N"] == 0)
+    # one zero column among independent ones: it alone deflates
+    X = np.array(m["Y"], order="F")
+    X[:, 1] = 0.0
+    out = solve(P, m["Q"], X, variant=variant)
+    assert out["t"] == s - 1 and np.all(out["N"][s - 1:] == 0)
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
