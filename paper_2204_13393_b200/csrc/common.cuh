@@ -19,6 +19,7 @@
 #include <unordered_map>
 
 #define PQR_DEV __device__ __forceinline__
+#define PQR_HOST_DEV __host__ __device__ __forceinline__
 
 namespace pqr {
 

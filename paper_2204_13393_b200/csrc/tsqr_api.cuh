@@ -47,10 +47,16 @@ int uw_for(int64_t rows) {
   return uw + (uw & 1);
 }
 int rp_for(int UW) { return kWyRowsPerUW * UW + 10; }  // >= rows + 1, = 10 (mod 16)
-size_t wy_smem(int RP, int wmax, int cap, int nbuf) { return wy_smem_bytes(RP, wmax, cap, nbuf); }
-int nbuf_for(int RP, int wmax, int cap) {
+// level kernels may use the whole 227 KB of dynamic shared memory per CTA
+constexpr size_t kWySmemBudget = 232448;
+// stage 1 (up) and stage 2 (down) kernels differ in groups x warps, hence in scratch
+size_t wy_smem(int RP, int wmax, int cap, int nbuf, bool up) {
+  return up ? wy_smem_bytes(RP, wmax, cap, nbuf, kWyUpWarps, kWyUpGroups)
+            : wy_smem_bytes(RP, wmax, cap, nbuf, kWyDownWarps, 1);
+}
+int nbuf_for(int RP, int wmax, int cap, bool up) {
   for (int nb = 4; nb > 2; --nb)
-    if (wy_smem(RP, wmax, cap, nb) <= (size_t)kSmemBudget) return nb;
+    if (wy_smem(RP, wmax, cap, nb, up) <= kWySmemBudget) return nb;
   return 2;
 }
 
@@ -113,7 +119,7 @@ WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
   L.q = lv.q; L.rem2 = lv.rem2; L.odd_last = lv.odd_last; L.nblocks = lv.nblocks;
   L.b0 = 0; L.nrun = lv.nblocks;
   L.V = lv.V; L.ldv = lv.ldv; L.T = lv.T; L.tstride = lv.tstride;
-  L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax; L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap);
+  L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax; L.nbuf = 2;  // set per kernel kind by the caller
   L.trace = wy_trace_buf();
   return L;
 }
@@ -128,7 +134,8 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   L.ovec = ((ts->cap & 1) == 0 && (ldo & 1) == 0 && aligned16(out)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
-  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
+  L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, true);
+  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, true);
   const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
 #define UPC(U, N, W) wy_up_t<U, N, W>(L, P, C, s, merge, mtoff, grid, smem, h->stream)
@@ -153,7 +160,8 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
   L.yvec = ((ldy & 1) == 0 && aligned16(Y)) ? 1 : 0;
   WyPanels P{pan, np};
   const int NT = ncol > 8 ? 2 : 1;
-  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf);
+  L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, false);
+  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, false);
   const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
 #define DNC(U, N, W) wy_down_t<U, N, W>(L, P, Call, t, ncol, grid, smem, h->stream)
@@ -300,7 +308,8 @@ int alloc_level(Ctx* h, TsqrLv& lv, int wmax, bool with_io) {
   int rc;
   lv.UW = uw_for(lv.q + 2 * (lv.rem2 > 0) + lv.odd_last);
   lv.RP = rp_for(lv.UW);
-  if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || wy_smem(lv.RP, wmax, ts->cap, 2) > (size_t)kSmemBudget) return PQR_EPLAN;
+  if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || std::max(wy_smem(lv.RP, wmax, ts->cap, 2, true), wy_smem(lv.RP, wmax, ts->cap, 2, false)) > kWySmemBudget)
+    return PQR_EPLAN;
   lv.tstride = (int64_t)32 * ts->cap;  // [0, 16 cap): per-panel T at 16*start; then merged-pair T
   if (lv.owns_v && (rc = dalloc(&lv.V, (size_t)lv.rows * ts->cap))) return rc;
   if (lv.owns_v && with_io) CUDA_TRY(cudaMemsetAsync(lv.V, 0, sizeof(double) * lv.rows * ts->cap, h->stream));

@@ -89,18 +89,28 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
   return (int)(L.q + (b < L.rem2 ? 2 : 0) + (b == L.nblocks - 1 ? L.odd_last : 0));
 }
 
+// per-group scratch (doubles) of a level kernel with NW consumer warps per group:
+// partials (NW + 1) E, Z (E), Householder-round buffers, diag, T scratch, round coefficients
+PQR_HOST_DEV constexpr int wy_group_scratch(int NW, int E) {
+  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 64;
+}
 // shared-memory bytes of a level kernel (host and device agree on this layout)
-inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf) {
-  const size_t E = (size_t)wmax * wmax;
-  return ((size_t)nbuf * (RP * wmax + 256) + (kWyWarps + 1) * E + E + kWyHH + 16 + 512 + 64) * sizeof(double) +
-         (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t);
+inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf, int NW, int NG) {
+  const int E = wmax * wmax;
+  return ((size_t)nbuf * (RP * wmax + 256) + (size_t)NG * wy_group_scratch(NW, E)) * sizeof(double) +
+         (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t) + 16;
 }
 
-template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false>
+// NG groups of NW consumer warps (+ the producer warpgroup).  With NG = 2 the groups take the
+// CTA's blocks alternately (group g: its blocks jb = g, g + 2, ...), each with its own scratch
+// and named barrier; the producer streams the items in block order as for one group, so while
+// one group runs its block's Householder tail the other applies its panels.
+template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false, int NG = 1>
 PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge_,
                      int mtoff) {
-  constexpr int NTH = 32 * NW, NLA = NTH + 128;  // consumer threads, launch size
+  constexpr int NTH = 32 * NW, NLA = NTH * NG + 128;  // consumer threads per group, launch size
   static_assert(NW == 8 || NW == 16, "consumer warps");
+  static_assert(NG == 1 || NG == 2, "groups");
   constexpr bool merge = MERGE;  // separate instantiation: the common path carries no merge code
   (void)merge_;
   extern __shared__ __align__(16) double sm[];
@@ -108,18 +118,25 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   const int RP = L.RP, nbuf = L.nbuf;
   const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
   const int E = wm * wm;
+  const int gtid = threadIdx.x, gwarp = gtid >> 5;
+  const int grp = NG > 1 ? (gwarp < NW ? 0 : 1) : 0;  // (producer warps: irrelevant)
+  const int GS = wy_group_scratch(NW, E);
   double* ring = sm;
-  double* red = ring + (size_t)nbuf * SS;  // E x (NW + 1): per-warp partials, entry-major (padded)
-  double* Zs = red + (kWyWarps + 1) * E;   // E: reduced Z (ld wm)
-  double* hred = Zs + E;                   // 2 x (NW*16 partials + 16 pivot-row values)
-  double* diagv = hred + kWyHH;            // 16: sigma*lambda of the new columns
+  double* red = ring + (size_t)nbuf * SS + grp * GS;  // E x (NW + 1): per-warp partials, entry-major (padded)
+  double* Zs = red + (NW + 1) * E;         // E: reduced Z (ld wm)
+  double* hred = Zs + E;                   // 2 x (NW*17 partials + 16 pivot-row values)
+  double* diagv = hred + 2 * (NW * kWyHS + 16);  // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
   double* hfc = tsc + 512;                 // 2 x 32: Householder-round coefficients (by round parity)
-  int4* pans = reinterpret_cast<int4*>(hfc + 64);
+  int4* pans = reinterpret_cast<int4*>(ring + (size_t)nbuf * SS + NG * GS);
   uint64_t* full = reinterpret_cast<uint64_t*>(pans + L.cap + 2);
   uint64_t* empty = full + nbuf;
+  // items issued by the producer so far (two groups: a group may run ahead of a slot's phase
+  // by more than one, so it first waits until its item has been issued, then on the parity)
+  volatile int* issued = reinterpret_cast<volatile int*>(empty + nbuf);
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // tid, warp: within the group
+  const int tid = gtid - grp * NTH, warp = tid >> 5, lane = gtid & 31;
   const int g = lane >> 2, q = lane & 3;
   const int np = P.np;
   const int ipb = np + (UP ? 1 : 0);  // ring items per block (stage 1: X first)
@@ -128,9 +145,10 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   const int64_t total = (int64_t)nb_cta * ipb;
 
   // never-copied slot parts must hold finite values (they meet zero coefficients)
-  for (int e = tid; e < nbuf * SS; e += NLA) ring[e] = 0.0;
-  for (int i = tid; i < np; i += NLA) pans[i] = P.pan[i];
-  if (tid == 0) {
+  for (int e = gtid; e < nbuf * SS; e += NLA) ring[e] = 0.0;
+  for (int i = gtid; i < np; i += NLA) pans[i] = P.pan[i];
+  if (gtid == 0) {
+    *issued = 0;
     for (int i = 0; i < nbuf; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NW);
@@ -142,9 +160,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 
   // ---- producer warp: streams ring item `it` into slot it % nbuf once the consumers have
   // released the slot's previous item (empty barrier, one arrival per consumer warp) ----
-  if (warp >= NW) {
-    if constexpr (NW == 16) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWyProducerRegs));
-    if (warp == NW && lane == 0) {
+  if (gwarp >= NW * NG) {
+    if constexpr (NW * NG == 16) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWyProducerRegs));
+    if (gwarp == NW * NG && lane == 0) {
       for (int it = 0; it < total; ++it) {
         const int jb = it / ipb;
         const int p = it - jb * ipb;
@@ -170,13 +188,17 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             bulk_g2s(buf + j * RP, L.V + (int64_t)(pn.x + j) * L.ldv + r0, (uint32_t)Rc * 8u, bar);
           bulk_g2s(buf + RP * wm, L.T + b * L.tstride + pn.z, tb, bar);
         }
+        if constexpr (NG > 1) {
+          __threadfence_block();
+          *issued = it + 1;
+        }
       }
     }
     return;
   }
-  if constexpr (NW == 16) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kWyConsumerRegs));
-  // consumer warps only from here: named barrier 1 over the NTH consumer threads
-  auto cbar = [&]() { asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory"); };
+  if constexpr (NW * NG == 16) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kWyConsumerRegs));
+  // consumer warps only from here: named barrier 1 + group over the group's NTH threads
+  auto cbar = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + grp), "n"(NTH) : "memory"); };
   // this warp is done with ring item `it` (all of its lanes' reads precede the arrival)
   auto release = [&](int64_t it) {
     __syncwarp();
@@ -231,7 +253,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 
   int64_t it = 0;  // consumer item cursor
   int hpar = 0;    // Householder-round buffer parity
-  for (int jb = 0; jb < nb_cta; ++jb) {
+  for (int jb = grp; jb < nb_cta; jb += NG) {
+    it = (int64_t)jb * ipb;  // this block's first ring item
     const int64_t b = L.b0 + blockIdx.x + (int64_t)jb * gridDim.x;
     const int64_t r0 = wy_start(L, b);
     const int R = wy_rows(L, b);
@@ -239,6 +262,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     double x[UW][NT][4];
     if (UP) {
       WY_TR(9);
+      if constexpr (NG > 1) {
+        while (*issued <= it) __nanosleep(32);
+      }
       mbar_wait(&full[it % nbuf], (uint32_t)((it / nbuf) & 1));
       WY_TR(0);
       const double* buf = ring + (size_t)(it % nbuf) * SS;
@@ -272,6 +298,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     // ---------------- committed panels ----------------
     for (int p = 0; p < np; ++p, ++it) {
       WY_TR(9);
+      if constexpr (NG > 1) {
+        while (*issued <= it) __nanosleep(32);
+      }
       mbar_wait(&full[it % nbuf], (uint32_t)((it / nbuf) & 1));
       WY_TR(0);
       const double* vb = ring + (size_t)(it % nbuf) * SS;
@@ -754,9 +783,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #undef WY_TR
 }
 
+// stage 1: NG = kWyUpGroups groups of 16 / NG warps (UW in 16-warp units, as planned by the host)
+#ifndef PQR_WY_UP_GROUPS
+#define PQR_WY_UP_GROUPS 2
+#endif
+constexpr int kWyUpGroups = PQR_WY_UP_GROUPS;
+constexpr int kWyUpWarps = kWyWarps / kWyUpGroups;  // consumer warps per group
 template <int UW, int NT, int WM, bool MERGE>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<kWyWarps, UW, NT, WM, true, MERGE>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<kWyUpWarps, UW * kWyUpGroups, NT, WM, true, MERGE, kWyUpGroups>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
