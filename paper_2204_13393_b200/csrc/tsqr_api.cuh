@@ -52,7 +52,7 @@ constexpr size_t kWySmemBudget = 232448;
 // stage 1 (up) and stage 2 (down) kernels differ in groups x warps, hence in scratch
 size_t wy_smem(int RP, int wmax, int cap, int nbuf, bool up) {
   return up ? wy_smem_bytes(RP, wmax, cap, nbuf, kWyUpWarps, kWyUpGroups)
-            : wy_smem_bytes(RP, wmax, cap, nbuf, kWyDownWarps, 1);
+            : wy_smem_bytes(RP, wmax, cap, nbuf, kWyDownWarps, kWyDownGroups);
 }
 int nbuf_for(int RP, int wmax, int cap, bool up) {
   for (int nb = 4; nb > 2; --nb)
@@ -81,7 +81,7 @@ cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int 
                       cudaStream_t st) {
   auto f = k_wy_down<UW, NT, WM>;
   ensure_smem(f, smem);
-  f<<<grid, 32 * kWyDownWarps + 128, smem, st>>>(L, P, Call, t, ncol);
+  f<<<grid, kWyDownLaunch, smem, st>>>(L, P, Call, t, ncol);
   return cudaGetLastError();
 }
 

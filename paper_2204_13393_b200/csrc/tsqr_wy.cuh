@@ -796,9 +796,14 @@ __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, i
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
 // (UW in 16-warp units, as planned by the host)
+#ifndef PQR_WY_DOWN_GROUPS
+#define PQR_WY_DOWN_GROUPS 2
+#endif
+constexpr int kWyDownGroups = PQR_WY_DOWN_GROUPS;
+constexpr int kWyDownLaunch = 32 * kWyDownWarps * kWyDownGroups + 128;
 template <int UW, int NT, int WM>
-__global__ void __launch_bounds__(32 * kWyDownWarps + 128, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  wy_body<kWyDownWarps, UW * kWyDownScale, NT, WM, false>(L, P, 0, t, Call, ncol, 0, 0);
+__global__ void __launch_bounds__(kWyDownLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
+  wy_body<kWyDownWarps, UW * kWyDownScale, NT, WM, false, false, kWyDownGroups>(L, P, 0, t, Call, ncol, 0, 0);
 }
 
 }  // namespace pqr
