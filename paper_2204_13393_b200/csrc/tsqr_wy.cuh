@@ -234,7 +234,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   // Compiled in only with -DPQR_WY_TRACE (tools: build.py --trace); absent from the product build.
 #ifdef PQR_WY_TRACE
   __shared__ unsigned long long s_tr[2][16];
-  const bool tr_on = L.trace != nullptr && blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == NW - 1);
+  const bool tr_on = L.trace != nullptr && blockIdx.x == 0 && grp == 0 && lane == 0 && (warp == 0 || warp == NW - 1);
   const int tr_w = warp == 0 ? 0 : 1;
   long long tr_t0 = 0;
   if (tr_on) {
