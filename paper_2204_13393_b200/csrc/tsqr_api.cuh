@@ -49,40 +49,58 @@ int uw_for(int64_t rows) {
 int rp_for(int UW) { return kWyRowsPerUW * UW + 10; }  // >= rows + 1, = 10 (mod 16)
 // level kernels may use the whole 227 KB of dynamic shared memory per CTA
 constexpr size_t kWySmemBudget = 232448;
-// stage 1 (up) and stage 2 (down) kernels differ in groups x warps, hence in scratch
-size_t wy_smem(int RP, int wmax, int cap, int nbuf, bool up) {
-  return up ? wy_smem_bytes(RP, wmax, cap, nbuf, kWyUpWarps, kWyUpGroups)
-            : wy_smem_bytes(RP, wmax, cap, nbuf, kWyDownWarps, kWyDownGroups);
+// kernels with NG groups of 16 / NG warps differ in scratch
+size_t wy_smem(int RP, int wmax, int cap, int nbuf, int NG) {
+  return wy_smem_bytes(RP, wmax, cap, nbuf, kWyWarps / NG, NG);
 }
-int nbuf_for(int RP, int wmax, int cap, bool up) {
+int nbuf_for(int RP, int wmax, int cap, int NG) {
   for (int nb = 4; nb > 2; --nb)
-    if (wy_smem(RP, wmax, cap, nb, up) <= kWySmemBudget) return nb;
+    if (wy_smem(RP, wmax, cap, nb, NG) <= kWySmemBudget) return nb;
   return 2;
 }
+// two groups when some CTA gets two or more blocks and a group's registers hold its rows
+// (UW <= 4 in 16-warp units, i.e. blocks of <= 1024 rows); PQR_WY_GROUPS=1|2 forces
+int groups_for(int64_t nrun, int sms, int UW) {
+  static const int env = getenv("PQR_WY_GROUPS") ? atoi(getenv("PQR_WY_GROUPS")) : 0;
+  if (env == 1 || env == 2) return env;
+  return nrun > sms && UW <= 4 ? 2 : 1;
+}
 
-template <int UW, int NT, int WM>
-cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
+template <int UW, int NT, int WM, int NG>
+cudaError_t wy_up_g(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
                     cudaStream_t st) {
   if constexpr (NT == 1 && WM == 8) {  // panel merges only pair 4-wide panels (s = 4)
     if (merge) {
-      auto f = k_wy_up<UW, NT, WM, true>;
+      auto f = k_wy_up<UW, NT, WM, true, NG>;
       ensure_smem(f, smem);
       f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
       return cudaGetLastError();
     }
   }
-  auto f = k_wy_up<UW, NT, WM, false>;
+  auto f = k_wy_up<UW, NT, WM, false, NG>;
   ensure_smem(f, smem);
   f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, 0, 0);
   return cudaGetLastError();
 }
 template <int UW, int NT, int WM>
-cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
+cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
+                    cudaStream_t st, int NG) {
+  return NG == 2 ? wy_up_g<UW, NT, WM, 2>(L, P, C, s, merge, mtoff, grid, smem, st)
+                 : wy_up_g<UW, NT, WM, 1>(L, P, C, s, merge, mtoff, grid, smem, st);
+}
+template <int UW, int NT, int WM, int NG>
+cudaError_t wy_down_g(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
                       cudaStream_t st) {
-  auto f = k_wy_down<UW, NT, WM>;
+  auto f = k_wy_down<UW, NT, WM, NG>;
   ensure_smem(f, smem);
-  f<<<grid, kWyDownLaunch, smem, st>>>(L, P, Call, t, ncol);
+  f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
   return cudaGetLastError();
+}
+template <int UW, int NT, int WM>
+cudaError_t wy_down_t(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
+                      cudaStream_t st, int NG) {
+  return NG == 2 ? wy_down_g<UW, NT, WM, 2>(L, P, Call, t, ncol, grid, smem, st)
+                 : wy_down_g<UW, NT, WM, 1>(L, P, Call, t, ncol, grid, smem, st);
 }
 
 // (UW, NT, WM) instantiations: WM = 16 levels have UW <= 2 (alloc_level)
@@ -134,11 +152,12 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   L.ovec = ((ts->cap & 1) == 0 && (ldo & 1) == 0 && aligned16(out)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
-  L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, true);
-  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, true);
+  const int NG = groups_for(L.nrun, h->sms, lv.UW);
+  L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, NG);
+  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, NG);
   const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
-#define UPC(U, N, W) wy_up_t<U, N, W>(L, P, C, s, merge, mtoff, grid, smem, h->stream)
+#define UPC(U, N, W) wy_up_t<U, N, W>(L, P, C, s, merge, mtoff, grid, smem, h->stream, NG)
   PQR_WY_SWITCH(lv.UW, NT, ts->wmax, UPC)
 #undef UPC
   wy_trace_dump("up", L, h->stream);
@@ -160,11 +179,12 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
   L.yvec = ((ldy & 1) == 0 && aligned16(Y)) ? 1 : 0;
   WyPanels P{pan, np};
   const int NT = ncol > 8 ? 2 : 1;
-  L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, false);
-  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, false);
+  const int NG = groups_for(L.nrun, h->sms, lv.UW);
+  L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, NG);
+  const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, NG);
   const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
-#define DNC(U, N, W) wy_down_t<U, N, W>(L, P, Call, t, ncol, grid, smem, h->stream)
+#define DNC(U, N, W) wy_down_t<U, N, W>(L, P, Call, t, ncol, grid, smem, h->stream, NG)
   PQR_WY_SWITCH(lv.UW, NT, ts->wmax, DNC)
 #undef DNC
   wy_trace_dump("down", L, h->stream);
@@ -308,7 +328,7 @@ int alloc_level(Ctx* h, TsqrLv& lv, int wmax, bool with_io) {
   int rc;
   lv.UW = uw_for(lv.q + 2 * (lv.rem2 > 0) + lv.odd_last);
   lv.RP = rp_for(lv.UW);
-  if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || std::max(wy_smem(lv.RP, wmax, ts->cap, 2, true), wy_smem(lv.RP, wmax, ts->cap, 2, false)) > kWySmemBudget)
+  if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || std::max(wy_smem(lv.RP, wmax, ts->cap, 2, 1), wy_smem(lv.RP, wmax, ts->cap, 2, 2)) > kWySmemBudget)
     return PQR_EPLAN;
   lv.tstride = (int64_t)32 * ts->cap;  // [0, 16 cap): per-panel T at 16*start; then merged-pair T
   if (lv.owns_v && (rc = dalloc(&lv.V, (size_t)lv.rows * ts->cap))) return rc;

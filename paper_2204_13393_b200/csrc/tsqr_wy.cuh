@@ -37,21 +37,14 @@
 
 namespace pqr {
 
-// Consumer warps: 16 in stage 1 (its Householder tail wants many lanes), 8 in stage 2 (measured
-// faster: cheaper barriers and partial sums, twice the rows and independent MMAs per warp).
-// UW below is per-warp units for the kernel's own warp count; the host plans in 16-warp units.
-#ifndef PQR_WY_DOWN_WARPS
-#define PQR_WY_DOWN_WARPS 8
-#endif
-constexpr int kWyWarps = 16;                     // stage-1 consumer warps (and the smem layout's maximum)
-constexpr int kWyDownWarps = PQR_WY_DOWN_WARPS;  // stage-2 consumer warps
-static_assert(kWyDownWarps == 8 || kWyDownWarps == 16, "stage-2 consumer warps");
-constexpr int kWyDownScale = kWyWarps / kWyDownWarps;  // stage-2 UW = host UW x this
-constexpr int kWyThreads = 32 * kWyWarps;        // stage-1 consumer threads
+// 16 consumer warps per CTA, as one group or as two groups of 8 on alternate blocks (see the
+// kernels at the end); UW below is per-warp units for the group's warp count, the host plans
+// in 16-warp units.
+constexpr int kWyWarps = 16;                     // consumer warps per CTA
+constexpr int kWyThreads = 32 * kWyWarps;        // consumer threads
 constexpr int kWyLaunch = kWyThreads + 128;      // + one producer warpgroup (one working lane)
-constexpr int kWyConsumerRegs = 112;  // setmaxnreg split of the 16-warp launch allocation
-                                      // (640 x 96): 4 x 128 x 112 + 128 x 24 <= 640 x 96; the
-                                      // 8-warp launch (384 x 168) needs no split
+constexpr int kWyConsumerRegs = 112;  // setmaxnreg split of the launch allocation (640 x 96):
+                                      // 4 x 128 x 112 + 128 x 24 <= 640 x 96
 constexpr int kWyProducerRegs = 24;
 constexpr int kWyRowsPerUW = 16 * kWyWarps;  // block rows covered per unit-per-warp
 constexpr int kWyMaxW = 16;                  // widest panel
@@ -783,27 +776,18 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #undef WY_TR
 }
 
-// stage 1: NG = kWyUpGroups groups of 16 / NG warps (UW in 16-warp units, as planned by the host)
-#ifndef PQR_WY_UP_GROUPS
-#define PQR_WY_UP_GROUPS 2
-#endif
-constexpr int kWyUpGroups = PQR_WY_UP_GROUPS;
-constexpr int kWyUpWarps = kWyWarps / kWyUpGroups;  // consumer warps per group
-template <int UW, int NT, int WM, bool MERGE>
+// Level kernels: NG groups of 16 / NG consumer warps (UW in 16-warp units, as planned by the
+// host).  NG = 2 when a CTA gets two or more blocks (one group's tail overlaps the other's
+// panels), NG = 1 (16 warps on one block: lower latency per block) for the small tree levels.
+template <int UW, int NT, int WM, bool MERGE, int NG>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<kWyUpWarps, UW * kWyUpGroups, NT, WM, true, MERGE, kWyUpGroups>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<kWyWarps / NG, UW * NG, NT, WM, true, MERGE, NG>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
-// (UW in 16-warp units, as planned by the host)
-#ifndef PQR_WY_DOWN_GROUPS
-#define PQR_WY_DOWN_GROUPS 2
-#endif
-constexpr int kWyDownGroups = PQR_WY_DOWN_GROUPS;
-constexpr int kWyDownLaunch = 32 * kWyDownWarps * kWyDownGroups + 128;
-template <int UW, int NT, int WM>
-__global__ void __launch_bounds__(kWyDownLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  wy_body<kWyDownWarps, UW * kWyDownScale, NT, WM, false, false, kWyDownGroups>(L, P, 0, t, Call, ncol, 0, 0);
+template <int UW, int NT, int WM, int NG>
+__global__ void __launch_bounds__(kWyLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
+  wy_body<kWyWarps / NG, UW * NG, NT, WM, false, false, NG>(L, P, 0, t, Call, ncol, 0, 0);
 }
 
 }  // namespace pqr
