@@ -22,4 +22,11 @@ print(big[-1] if big else 0)
 PY
 )
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wy_down -s $SKIP -c 1 -o gpurun_out/${TAG}_wy_down $T > gpurun_out/${TAG}_wy_down.log 2>&1
+# summaries on the box (the .ncu-rep files are large: gpurun copies back <= 64 MiB)
+python tools/ncu_summary.py gpurun_out/${TAG}_wy_up.ncu-rep gpurun_out/${TAG}_wy_down.ncu-rep gpurun_out/${TAG}_cholqr.ncu-rep > gpurun_out/${TAG}_ncu_full.json 2> gpurun_out/${TAG}_ncu_summary.err
+python tools/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launches_summary.csv 2>/dev/null
+for k in wy_up wy_down; do
+  ncu -i gpurun_out/${TAG}_$k.ncu-rep --page source --csv --print-source cuda,sass 2>/dev/null | python tools/ncu_lines.py 40 > gpurun_out/${TAG}_${k}_lines.txt
+done
+rm -f gpurun_out/${TAG}_cholqr.ncu-rep gpurun_out/${TAG}_launches.csv
 ls -la gpurun_out | grep ${TAG}
