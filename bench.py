@@ -221,6 +221,7 @@ def main():
     ap.add_argument("--variant", default="both", choices=["cholqr2", "tsqr", "both"])
     ap.add_argument("--impl", default="pqr", choices=["pqr", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-serial", action="store_true", help="e2e: the variants one after the other only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -274,10 +275,13 @@ def main():
     sharded = args.workload == "weak" and world > 1
     variants = ["cholqr2", "tsqr"] if args.variant == "both" else [args.variant]
     handles = {}
+    # one CUDA stream per variant's handle (the calls are host-synchronous, so the device loop
+    # is sequential; the e2e leg runs the two handles from two host threads)
+    hstreams = {v: torch.cuda.Stream(device) for v in variants}
     for v in variants:
         # one ncclUniqueId per communicator (each handle owns one)
         nccl_id = pdist.nccl_id_for_library(world) if sharded else None
-        handles[v] = pqr.PQR(n, k, s, Q, variant=v, stream=stream, rank=rank if sharded else 0,
+        handles[v] = pqr.PQR(n, k, s, Q, variant=v, stream=hstreams[v], rank=rank if sharded else 0,
                              nranks=world if sharded else 1, nccl_id=nccl_id)
     del Q
     torch.cuda.empty_cache()
@@ -291,10 +295,10 @@ def main():
             if timing["on"]:
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
+                a.record(hstreams[v])
             ts.append(handles[v].solve(X, U=U, P=Pm, N=Nm, flags=pqr.PQR_NO_APPEND))
             if timing["on"]:
-                b.record(stream)
+                b.record(hstreams[v])
                 b.synchronize()
                 var_ms[v] += a.elapsed_time(b)
         return ts
@@ -314,10 +318,10 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     timing["on"] = True
     with ClockSampler(local_rank) as clk:
-        ev0.record(stream)
+        ev0.record(hstreams[variants[0]])
         for _ in range(args.steps):
             t_vals = step()
-        ev1.record(stream)
+        ev1.record(hstreams[variants[-1]])  # after the last (host-synchronous) call
         torch.cuda.synchronize()
     barrier()
     ms = ev0.elapsed_time(ev1)
@@ -368,31 +372,69 @@ def main():
     frac_whole = t_roof / ms_step
 
     # ---- e2e through the C-ABI with HOST buffers (pinned), copies inside the timed region ----
+    # Every step uploads X and downloads U (and P, N) per variant.  Default: the step's two
+    # independent solves run from two host threads (one per variant), so one solve's U download
+    # overlaps the other's X upload on the full-duplex link; "serial" runs them one after the
+    # other (also reported).
     e2e = None
     if args.e2e_steps > 0:
         Xh = torch.empty((s, n), dtype=torch.float64, pin_memory=True).t()
         Xh.copy_(X)
-        Uh = torch.empty((s, n), dtype=torch.float64, pin_memory=True).t()
-        Ph = torch.empty((s, k), dtype=torch.float64, pin_memory=True).t()
-        Nh = torch.empty((s, s), dtype=torch.float64, pin_memory=True).t()
+        outs = {}
         for v in variants:
+            outs[v] = (torch.empty((s, n), dtype=torch.float64, pin_memory=True).t(),
+                       torch.empty((s, k), dtype=torch.float64, pin_memory=True).t(),
+                       torch.empty((s, s), dtype=torch.float64, pin_memory=True).t())
+
+        def solve_host(v):
+            Uh, Ph, Nh = outs[v]
             handles[v].solve(Xh, U=Uh, P=Ph, N=Nh, flags=pqr.PQR_NO_APPEND)
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            for v in variants:
-                handles[v].solve(Xh, U=Uh, P=Ph, N=Nh, flags=pqr.PQR_NO_APPEND)
-        torch.cuda.synchronize()
-        dt = torch.tensor([time.perf_counter() - t0], device=device, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e_step = float(dt.item()) / args.e2e_steps
+
+        def run_serial(steps):
+            for _ in range(steps):
+                for v in variants:
+                    solve_host(v)
+
+        def run_threads(steps):
+            errs = []
+
+            def worker(v):
+                try:
+                    for _ in range(steps):
+                        solve_host(v)
+                except Exception as e:  # pragma: no cover
+                    errs.append(e)
+
+            ths = [threading.Thread(target=worker, args=(v,)) for v in variants]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            if errs:
+                raise errs[0]
+
+        def timed(fn):
+            fn(1)  # warm-up (staging buffers, copy streams)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn(args.e2e_steps)
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t0], device=device, dtype=torch.float64)
+            if world > 1:
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            return float(dt.item()) / args.e2e_steps
+
+        serial_step = timed(run_serial)
+        conc = len(variants) > 1 and not args.e2e_serial
+        e2e_step = timed(run_threads) if conc else serial_step
         e2e = {"value": mand / e2e_step / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 8 * n * s * len(variants),
                "d2h_bytes_per_step": (8 * n * s + 8 * k * s + 8 * s * s) * len(variants),
-               "ms_per_step": e2e_step * 1e3}
-        del Xh, Uh
+               "ms_per_step": e2e_step * 1e3,
+               "mode": "concurrent: one host thread per variant" if conc else "serial",
+               "serial": {"value": mand / serial_step / 1e9, "ms_per_step": serial_step * 1e3}}
+        del Xh, outs
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:

@@ -225,6 +225,45 @@ def test_host_pipeline(P, orc, variant, chunks, n, monkeypatch):
         assert rel(hst[key], dv[key]) < 1e-12, key
 
 
+def test_two_handles_two_threads(P, orc):
+    """Two handles (one per variant, each on its own stream) called concurrently from two host
+    threads with host buffers — the bench's e2e leg — give the serial results."""
+    import threading
+
+    import torch
+
+    n, k, s = 300_000, 16, 8
+    Q = inputs.orthonormal(181, n, k)
+    X = inputs.gaussian(182, n, s)
+    ref = orc.householder_pqr(Q, X)
+    hs = {v: P.PQR(n, k, s, dev(Q), variant=v, stream=torch.cuda.Stream()) for v in VARIANTS}
+    res = {}
+
+    def run(v, reps):
+        out = []
+        for _ in range(reps):
+            U = np.zeros((n, s), order="F")
+            Pm = np.zeros((k, s), order="F")
+            Nm = np.zeros((s, s), order="F")
+            t = hs[v].solve(X, U=U, P=Pm, N=Nm, flags=P.PQR_NO_APPEND)
+            out.append((t, U, Pm, Nm))
+        res[v] = out
+
+    ths = [threading.Thread(target=run, args=(v, 3)) for v in VARIANTS]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for v in VARIANTS:
+        hs[v].close()
+        assert len(res[v]) == 3
+        for t, U, Pm, Nm in res[v]:
+            assert t == s
+            assert rel(Pm, ref["P"]) < 1e-10 and rel(Nm, ref["N"]) < 1e-10 and rel(U, ref["U"]) < 1e-10
+        # repeated concurrent calls are bitwise reproducible
+        assert all(np.array_equal(res[v][0][1], r[1]) for r in res[v][1:])
+
+
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_no_deflation_flag_breakdown(P, variant):
     n, k, s = 4000, 8, 4
