@@ -658,6 +658,10 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const char* e = getenv("PQR_SMS")) {  // testing aid: size grids for fewer SMs (sanitizer runs)
+    const int v = atoi(e);
+    if (v >= 1 && v < h->sms) h->sms = v;
+  }
   h->cap = cfg->k_max + cfg->s_max;
   h->ld = (cfg->n_local + 1) & ~int64_t(1);  // even leading dimension: 16-byte row pairs
   const int64_t n = cfg->n_local;

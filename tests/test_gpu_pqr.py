@@ -225,6 +225,39 @@ def test_host_pipeline(P, orc, variant, chunks, n, monkeypatch):
         assert rel(hst[key], dv[key]) < 1e-12, key
 
 
+@pytest.mark.parametrize("sms", ["2", "3"])
+def test_tsqr_two_groups_many_blocks_per_cta(P, orc, sms, monkeypatch):
+    """Grids sized for 2-3 SMs (PQR_SMS) give every CTA several leaf blocks, so both groups of
+    the two-group level kernels work, hand ring slots back and forth and run ahead of each
+    other; the panel merge (s = 4 after s = 4) runs too.  Parity with the oracle on every call
+    and bitwise reproducibility over repeated runs (a race would show up here)."""
+    import torch
+
+    monkeypatch.setenv("PQR_SMS", sms)
+    n, k = 23 * 1024 + 41, 24
+    Q = inputs.orthonormal(191, n, k)
+    Xs = [inputs.gaussian(192 + i, n, s) for i, s in enumerate((8, 4, 4))]
+    runs = []
+    for rep in range(2):
+        outs = []
+        with P.PQR(n, k + 16, 8, dev(Q), k=k, variant="tsqr") as h:
+            Qcur = Q
+            for X in Xs:
+                s = X.shape[1]
+                U = empty(n, s)
+                Pm, Nm = empty(Qcur.shape[1], s), empty(s, s)
+                t = h.solve(dev(X), U=U, P=Pm, N=Nm, s=s)
+                torch.cuda.synchronize()
+                ref = orc.householder_pqr(Qcur, X)
+                assert t == s
+                assert rel(host(Pm), ref["P"]) < 1e-10 and rel(host(U)[:, :t], ref["U"]) < 1e-10
+                outs.append(host(U))
+                Qcur = np.asfortranarray(np.hstack([Qcur, ref["U"]]))
+        runs.append(outs)
+    for a, b in zip(runs[0], runs[1]):
+        assert np.array_equal(a, b)
+
+
 def test_two_handles_two_threads(P, orc):
     """Two handles (one per variant, each on its own stream) called concurrently from two host
     threads with host buffers — the bench's e2e leg — give the serial results."""
