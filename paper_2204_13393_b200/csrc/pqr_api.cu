@@ -658,7 +658,7 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
-  if (const char* e = getenv("PQR_SMS")) {  // testing aid: size grids for fewer SMs (sanitizer runs)
+  if (const char* e = getenv("PQR_SMS")) {  // testing aid: size grids for fewer SMs (several blocks per CTA)
     const int v = atoi(e);
     if (v >= 1 && v < h->sms) h->sms = v;
   }
