@@ -23,9 +23,15 @@
  *  - Matrix pointers may be DEVICE pointers (cudaMalloc'd, the fast path) or HOST
  *    pointers (pageable or pinned); the library detects host memory with
  *    cudaPointerGetAttributes and stages it through handle-owned device buffers on
- *    the handle's stream.  The caller owns every pointer it passes.
+ *    the handle's stream.  With both X and U on the host (one rank, from 2^18 rows) the
+ *    staging is pipelined: row chunks move on a second, handle-owned copy stream while
+ *    the first and last passes run chunk by chunk.  The caller owns every pointer it
+ *    passes.
  *  - Every call is ordered on the handle's stream (pqr_config.stream).  Calls that
- *    return a host scalar (t) synchronise that stream before returning.
+ *    return a host scalar (t) synchronise that stream (and the copy stream) before
+ *    returning.
+ *  - Handles share no mutable state: distinct handles (each with its own stream) may
+ *    be called concurrently from different host threads; one handle must not be.
  *  - Multi-GPU: one process per GPU; every rank calls every function collectively
  *    with its own contiguous row shard (n_local rows).  P, N and t are replicated
  *    (bitwise identical) on all ranks.
