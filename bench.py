@@ -426,7 +426,9 @@ def main():
             return float(dt.item()) / args.e2e_steps
 
         serial_step = timed(run_serial)
-        conc = len(variants) > 1 and not args.e2e_serial
+        # (sharded runs stay serial: two NCCL communicators driven from two threads could
+        # interleave their collectives differently on different ranks)
+        conc = len(variants) > 1 and not args.e2e_serial and not sharded
         e2e_step = timed(run_threads) if conc else serial_step
         e2e = {"value": mand / e2e_step / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 8 * n * s * len(variants),
