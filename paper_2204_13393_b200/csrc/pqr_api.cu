@@ -378,9 +378,11 @@ int run_update(int64_t n, int k, const double* Q, int64_t ldq, int sx, const dou
                    (ldu & 1) == 0 && aligned16(U);
   const int64_t nslab = (n + 15) / 16;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 6, (nslab + 7) / 8));
-  static const int env_cw = getenv("PQR_UPD_CW") ? atoi(getenv("PQR_UPD_CW")) : 16;
+  // column chunk of the stages: 32 from m = 128 (weak config: 6.28 -> 6.14 ms), else 16
+  // (k = 64: 16 is faster); PQR_UPD_CW forces
+  static const int env_cw = getenv("PQR_UPD_CW") ? atoi(getenv("PQR_UPD_CW")) : 0;
   static const int env_ctas = getenv("PQR_UPD_CTAS") ? atoi(getenv("PQR_UPD_CTAS")) : 2;
-  const int CW = env_cw == 16 ? 16 : 32;
+  const int CW = env_cw == 16 ? 16 : env_cw == 32 ? 32 : (m >= 128 ? 32 : 16);
   const int ctas = env_ctas == 2 ? 2 : 1;
   const int nch = (m + CW - 1) / CW;
   const size_t smM = (size_t)NT * nch * CW * 8 * sizeof(double);
