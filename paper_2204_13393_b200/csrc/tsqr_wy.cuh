@@ -2,10 +2,12 @@
 // reduction subalgorithms), persistent, with blocked (compact-WY) reflector panels and
 // fp64 MMAs (mma.sync m8n8k4 .f64, SASS DMMA).
 //
-// Blocks of a level (leaf row blocks, or tree nodes) are processed by a persistent grid
-// (one CTA per SM: NW = 16 consumer warps in stage 1, 8 in stage 2, plus a producer
-// warpgroup; CTA i takes blocks i, i + grid, ...).  A block holds R <= 16*NW*UW rows;
-// consumer warp w owns UW units of 16 rows, lane (g = l>>2, q = l&3)
+// Blocks of a level (leaf row blocks, or tree nodes) are processed by a persistent grid of
+// 640-thread CTAs (one per SM): 16 consumer warps plus a producer warpgroup; CTA i takes
+// blocks i, i + grid, ...  The consumer warps form NG groups of NW = 16 / NG warps: one group
+// per block (NG = 1, small tree levels), or two groups on alternate blocks of the CTA
+// (NG = 2), so that one group's Householder tail overlaps the other group's panels.  A block
+// holds R <= 16*NW*UW rows; group warp w owns UW units of 16 rows, lane (g = l>>2, q = l&3)
 // keeping rows 16u+4q+{0..3} of columns 8nt+g in registers (the D-fragment layout of the
 // update MMA below).  The block's reflectors are grouped in panels (the s reflectors one
 // call creates, or one LOR-build chunk): H_a ... H_b = I - V T V^T with
@@ -16,22 +18,23 @@
 //
 // Memory: everything a block streams (its X — stage 1 only — and every panel V with its
 // T) is a "ring item", copied by cp.async.bulk into one of nbuf shared-memory slots and
-// completed on that slot's mbarrier.  One producer lane keeps nbuf items in flight
+// completed on that slot's mbarrier.  One producer lane streams the items in block order,
 // across block boundaries, so the next block's data lands while this block does its
-// Householder tail; a slot is refilled only after the block-wide barrier that proves
-// every warp has finished the item it held.
+// Householder tail; a slot is refilled once every warp of the group that held it released
+// it (empty mbarrier).
 //
-// Per panel: Gram Z = V^T x (per-warp DMMA partials) -> barrier -> fixed-order sum of
-// the 16 partials by |Z| threads -> barrier -> every warp forms Z'^T = Z^T T (or Z^T T^T)
-// with two DMMAs from shared memory -> update x^T -= Z'^T V^T.  Two barriers per panel.
+// Per panel: Gram Z = V^T x (per-warp DMMA partials) -> group barrier -> fixed-order sum of
+// the NW partials -> group barrier -> every warp forms Z'^T = Z^T T (or Z^T T^T) with two
+// DMMAs from shared memory -> update x^T -= Z'^T V^T.  Two barriers per panel.
 //
 // Stage-1 tail (Alg. 6 lines 2-9 on rows C..R-1 of the s new columns; never deflating,
-// reading R4): the columns stay in registers.  Round c makes one block-wide reduction of
-// D_c' = x_c . x_c' over rows >= r = C+c for all c' >= c (c' = c gives lambda^2) and
-// broadcasts row r; then every lane knows the reflector
+// reading R4): the columns move to a row layout (lane-local rows).  Round c makes one
+// group-wide reduction of D_c' = x_c . x_c' over rows >= r = C+c for all c' (c' = c gives
+// lambda^2) and broadcasts row r; warp 0 forms the reflector
 //   v = (x_c - sigma*lambda e_r) / sqrt(2 lambda (lambda + |x_c[r]|)),  sigma = -sgn(x_c[r]),
-// and v . x_c' = (D_c' - sigma*lambda x_c'[r]) / sqrt(...), so one barrier per column.
-// Then T of the new panel from V^T V (one more reduction), and the outputs.
+// and the coefficients v . x_c' = (D_c' - sigma*lambda x_c'[r]) / sqrt(...) (c' > c: update;
+// c' < c: column c of V^T V for T) behind a second barrier.  Then T of the new panel and the
+// outputs.
 #pragma once
 #include "common.cuh"
 
