@@ -150,14 +150,15 @@ def oracle_sample(w, target_s=15.0, max_rows=None):
 
     k, s = w["k"], w["s"]
     n_full = w["n"]
-    rows = min(n_full, 2 ** 14)
+    # calibration run: large enough for the oracle's threads to scale as on the real sample
+    rows = min(n_full, 2 ** 14 if target_s < 2 else 2 ** 17)
     Q = inputs.orthonormal(SEED + 11, rows, k)
     X = inputs.gaussian(SEED + 12, rows, s)
     t0 = time.perf_counter()
     oracle.householder_pqr(Q, X)
     dt = time.perf_counter() - t0
-    # scale the sample to ~target_s seconds (the oracle is O(n) per call)
-    rows2 = int(min(n_full, max(rows, rows * target_s / max(dt, 1e-3) * 0.8)))
+    # scale the sample to ~target_s seconds (the oracle is O(n) per call); at most 2^23 rows
+    rows2 = int(min(n_full, 2 ** 23, max(rows, rows * target_s / max(dt, 1e-3) * 0.9)))
     if max_rows:
         rows2 = min(rows2, max_rows)
     if rows2 > rows:
