@@ -552,6 +552,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     }
     double* Gs = tsc;  // strict upper part of V^T V (ld 16), column c written in round c by tid 0
     WY_TR(10);
+    if constexpr (S8 == 8) {
 #pragma unroll
     for (int c = 0; c < S8; ++c) {
       if (c >= s) break;
@@ -637,6 +638,101 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-hf[cc], vv, xr[e][cc]);
           xr[e][c] = vv;
         }
+    }
+    } else {
+    // 16 columns: the rounds stay a loop (fully unrolled they overflow the instruction cache);
+    // column c of a row is picked with a select chain instead of a dynamic register index
+#pragma unroll 1
+    for (int c = 0; c < S8; ++c) {
+      if (c >= s) break;
+      const int r = C + c;
+      double xc[RPL];
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        double v = 0.0;
+#pragma unroll
+        for (int cc = 0; cc < S8; ++cc) v = cc == c ? xr[e][cc] : v;
+        xc[e] = v;
+      }
+      double D[S8];
+#pragma unroll
+      for (int cc = 0; cc < S8; ++cc) D[cc] = 0.0;
+#pragma unroll
+      for (int e = 0; e < RPL; ++e)
+        if (rowk[e] >= r) {
+#pragma unroll
+          for (int cc = 0; cc < S8; ++cc) D[cc] = fma(xc[e], xr[e][cc], D[cc]);
+        }
+#pragma unroll
+      for (int mb = 16, w = S8; w > 1; mb >>= 1, w >>= 1) {
+        const bool up = (lane & mb) != 0;
+#pragma unroll
+        for (int j = 0; j < w / 2; ++j) {
+          const double send = up ? D[j] : D[j + w / 2];
+          const double keep = up ? D[j + w / 2] : D[j];
+          D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
+        }
+      }
+      constexpr int LG = S8 == 8 ? 4 : 2;
+      D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
+      if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
+      const int vi = (lane / LG) & (S8 - 1);
+      double* hb = hred + hpar * (NW * kWyHS + 16);
+      hpar ^= 1;
+      if ((lane & (LG - 1)) == 0) hb[warp * kWyHS + vi] = D[0];
+#pragma unroll
+      for (int e = 0; e < RPL; ++e)
+        if (rowk[e] == r) {
+#pragma unroll
+          for (int cc = 0; cc < S8; ++cc) hb[NW * kWyHS + cc] = xr[e][cc];
+        }
+      WY_TR(11);
+      cbar();
+      WY_TR(12);
+      double* hf = hfc + (c & 1) * 32;
+      if (warp == 0) {
+        constexpr int NP = 32 / S8, WPP = NW / NP;
+        const int v = lane & (S8 - 1), part = lane / S8;
+        const double* hv = hb + part * WPP * kWyHS + v;
+        double tot = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
+#pragma unroll
+        for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
+        const double lam2 = __shfl_sync(0xffffffffu, tot, c);
+        const double u0 = hb[NW * kWyHS + c];
+        const double lam = sqrt(lam2);
+        const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;
+        const double diag = sigma * lam;
+        const double nv2 = 2.0 * lam * (lam + fabs(u0));
+        const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;
+        const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[NW * kWyHS + v]);
+        if (lane < S8) {
+          hf[lane] = fv;
+          if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
+        }
+        if (lane == 0) {
+          hf[S8] = inv;
+          hf[S8 + 1] = u0 - diag;
+          diagv[c] = diag;
+        }
+      }
+      WY_TR(14);
+      cbar();
+      WY_TR(15);
+      const double inv = hf[S8], wr = hf[S8 + 1];
+      WY_TR(13);
+#pragma unroll
+      for (int e = 0; e < RPL; ++e)
+        if (rowk[e] >= r) {
+          const double vv = (rowk[e] == r ? wr : xc[e]) * inv;
+#pragma unroll
+          for (int cc = 0; cc < S8; ++cc) {
+            if (cc > c) xr[e][cc] = fma(-hf[cc], vv, xr[e][cc]);
+            else if (cc == c) xr[e][cc] = vv;
+          }
+        }
+    }
     }
     WY_TR(7);
     // ---------------- T of the new panel: T^{-1} = I/2 + striu(V^T V) (warp 0) ----------------
