@@ -314,11 +314,13 @@ int run_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double
              int64_t* launches) {
   const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (ldx & 1) == 0 && aligned16(X);
   static const int env_rb = getenv("PQR_GRAM_RB") ? atoi(getenv("PQR_GRAM_RB")) : 32;
-  static const int env_ctas = getenv("PQR_GRAM_CTAS") ? atoi(getenv("PQR_GRAM_CTAS")) : 1;
+  // two CTAs per SM (two stages each) beat one CTA with five stages for wide [Q X] (weak
+  // config -1.5 %, config D -5 %), one CTA is faster at m = 72 (config S); PQR_GRAM_CTAS forces
+  static const int env_ctas = getenv("PQR_GRAM_CTAS") ? atoi(getenv("PQR_GRAM_CTAS")) : 0;
   const int RB = env_rb == 32 ? 32 : 16;
-  const int ctas = env_ctas == 1 ? 1 : 2;
   const int groups = kCpaWarps / (RB / 8);
   const int m = k + s, MT = (m + 7) / 8, MTH = (MT + groups - 1) / groups, NT = s > 8 ? 2 : 1;
+  const int ctas = env_ctas == 1 ? 1 : env_ctas == 2 ? 2 : (m >= 100 ? 2 : 1);
   const size_t stage_bytes = (size_t)MT * 8 * (RB + 8) * sizeof(double);
   const size_t red_bytes = (size_t)kCpaWarps * MTH * NT * 64 * sizeof(double);
   const size_t budget = ctas == 2 ? kSmemBudget / 2 - 2048 : kSmemBudget;
@@ -326,7 +328,7 @@ int run_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double
   while (NS >= 2 && (size_t)NS * stage_bytes < red_bytes) ++NS;
   const size_t smem = std::max((size_t)NS * stage_bytes, red_bytes) + 2 * NS * sizeof(uint64_t);
   cudaError_t e;
-  if (vec && MTH <= 10 && NS >= 3 && smem <= budget) {
+  if (vec && MTH <= 10 && NS >= (ctas == 2 ? 2 : 3) && smem <= budget) {
     GramCpaArgs a{};
     a.Q = Q; a.ldq = ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.NS = NS;
     a.partials = partials; a.W = W; a.ldw = ldw; a.ticket = ticket;
