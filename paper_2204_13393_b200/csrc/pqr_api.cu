@@ -274,13 +274,15 @@ GramPlan plan_gram(int64_t n, int k, int s, int sms) {
 
 template <int MTW, int NT>
 cudaError_t launch_gram_t(const GramPlan& p, const GramArgs& a, bool vec, cudaStream_t st) {
+  // (always raise the limit: 48 KB of dynamic plus the kernel's static shared memory is
+  // already over the default)
   if (vec) {
     auto f = k_gram<MTW, NT, true>;
-    if (p.smem > 48 * 1024) ensure_smem(f, p.smem);
+    ensure_smem(f, p.smem);
     f<<<p.grid, kThreads, p.smem, st>>>(a);
   } else {
     auto f = k_gram<MTW, NT, false>;
-    if (p.smem > 48 * 1024) ensure_smem(f, p.smem);
+    ensure_smem(f, p.smem);
     f<<<p.grid, kThreads, p.smem, st>>>(a);
   }
   return cudaGetLastError();

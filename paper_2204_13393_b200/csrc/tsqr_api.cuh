@@ -359,6 +359,12 @@ int tsqr_alloc(Ctx* h) {
   nb = std::max(nb, 2 * cap);
   if (nb < cap || n < cap) return PQR_EPLAN;
   int64_t p0 = std::max<int64_t>(1, (n + nb - 1) / nb);
+  // the largest block (q, + 2 for the first rem2 blocks, + 1 odd row) must not exceed nb
+  auto max_rows = [&](int64_t p) {
+    const int64_t q = (n / p) & ~int64_t(1), rest = n - p * q;
+    return q + (rest / 2 > 0 ? 2 : 0) + (rest & 1);
+  };
+  while (max_rows(p0) > nb && (n / (p0 + 1)) >= cap) ++p0;
   while (p0 > 1 && ((n / p0) & ~int64_t(1)) < cap) --p0;
   TsqrLv leaf;
   leaf.nblocks = (int)p0;

@@ -54,7 +54,10 @@ def check_vs_oracle(out, ref, tol=1e-10):
 @pytest.mark.parametrize("n,k,s", [(10_000, 32, 4), (4097, 13, 3), (20_000, 0, 8), (65_536, 128, 8),
                                    (30_001, 96, 16), (12, 3, 2), (300_007, 64, 8),
                                    (20_011, 144, 16), (50_000, 152, 8),  # these two: k + s = kMMax
-                                   (7777, 5, 1), (1000, 0, 1), (2049, 40, 7)])
+                                   (7777, 5, 1), (1000, 0, 1), (2049, 40, 7),
+                                   # odd n (odd ld: unaligned Gram path) with s > 8 and a 48 KB
+                                   # reduction buffer; leaf remainders that overflow a 512-row block
+                                   (20_001, 74, 9), (20_001, 28, 13), (105_253, 92, 14)])
 def test_vs_oracle_random(P, orc, variant, n, k, s):
     Q = inputs.orthonormal(7 + n, n, k)
     X = inputs.gaussian(8 + n, n, s)
