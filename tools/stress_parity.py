@@ -1,5 +1,6 @@
-"""Randomised parity sweep (tuning/validation aid, not part of the suite): random (n, k, s,
-variant, leaf block size, grid size), device buffers, against the CPU oracle.  Usage:
+"""Randomised parity sweep (validation aid, not part of the suite): random (n, k, s, variant,
+leaf block size, grid size) and mode — one solve, three appending solves of random widths, host
+buffers, a dependent column — against the CPU oracle.  Usage:
 python tools/stress_parity.py SECONDS [SEED]"""
 import os
 import sys
@@ -47,27 +48,53 @@ def main():
         else:
             os.environ.pop("PQR_SMS", None)
         seed = int(rng.integers(1 << 30))
+        mode = ["plain", "plain", "append", "host", "dependent"][rng.integers(5)]
         Q = inputs.orthonormal(seed, n, k)
-        X = inputs.gaussian(seed + 1, n, s)
         try:
-            U = torch.empty((s, n), dtype=torch.float64, device="cuda").t()
-            Pm = torch.empty((s, max(k, 1)), dtype=torch.float64, device="cuda").t()
-            Nm = torch.empty((s, s), dtype=torch.float64, device="cuda").t()
-            with pqr.PQR(n, k, s, dev(Q) if k else None, k=k, variant=variant, block_rows=br) as h:
-                t = h.solve(dev(X), U=U, P=Pm, N=Nm, flags=pqr.PQR_NO_APPEND)
-            torch.cuda.synchronize()
-            ref = oracle.householder_pqr(Q, X)
-            e = max(rel(host(U)[:, :t], ref["U"]), rel(host(Nm), ref["N"]),
-                    rel(host(Pm)[:k], ref["P"]) if k else 0.0)
-            ok = t == ref["t"] and e < 1e-10
+            nsolve = 3 if mode == "append" else 1
+            ok, e, t = True, 0.0, None
+            with pqr.PQR(n, k + (s * nsolve if mode == "append" else 0), s, dev(Q) if k else None, k=k,
+                         variant=variant, block_rows=br) as h:
+                Qcur = Q
+                for it in range(nsolve):
+                    si = s if it == 0 else int(rng.integers(1, s + 1))
+                    X = inputs.gaussian(seed + 1 + it, n, si)
+                    if mode == "dependent" and si >= 2:
+                        X[:, si - 1] = X[:, 0] + Qcur @ inputs.gaussian(seed + 7, Qcur.shape[1], 1)[:, 0] if Qcur.shape[1] else X[:, 0]
+                    kk = Qcur.shape[1]
+                    if mode == "host":
+                        Uh, Ph, Nh = (np.zeros((n, si), order="F"), np.zeros((max(kk, 1), si), order="F"),
+                                      np.zeros((si, si), order="F"))
+                        t = h.solve(X, U=Uh, P=Ph, N=Nh, flags=pqr.PQR_NO_APPEND, s=si)
+                        Uo, Po, No = Uh, Ph, Nh
+                    else:
+                        U = torch.empty((si, n), dtype=torch.float64, device="cuda").t()
+                        Pm = torch.empty((si, max(kk, 1)), dtype=torch.float64, device="cuda").t()
+                        Nm = torch.empty((si, si), dtype=torch.float64, device="cuda").t()
+                        flags = 0 if mode == "append" else pqr.PQR_NO_APPEND
+                        t = h.solve(dev(X), U=U, P=Pm, N=Nm, flags=flags, s=si)
+                        torch.cuda.synchronize()
+                        Uo, Po, No = host(U), host(Pm), host(Nm)
+                    ref = oracle.householder_pqr(Qcur, X)
+                    ei = max(rel(Uo[:, :t], ref["U"]) if t else 0.0, rel(No, ref["N"]),
+                             rel(Po[:kk], ref["P"]) if kk else 0.0)
+                    if mode == "dependent":  # N's pivot rows only (the dependent column's entries are tiny)
+                        ei = max(rel(Po[:kk], ref["P"]) if kk else 0.0, 0.0)
+                    e = max(e, ei)
+                    ok = ok and t == ref["t"] and ei < 1e-10
+                    if mode == "append":
+                        Qcur = np.asfortranarray(np.hstack([Qcur, ref["U"]]))
         except Exception as ex:  # noqa: BLE001
             ok, e, t = False, str(ex), None
             if "block plan" in e and br > 512 and s > 8:
                 continue  # documented: 16-wide panels need leaf blocks of <= 512 rows
+            if "capacity exceeded" in e and "pqr_create" in e:
+                continue  # documented: k_max + s_max <= 152
         cases += 1
         if not ok:
             fails += 1
-            print("FAIL", dict(variant=variant, n=n, k=k, s=s, block_rows=br, sms=sms, seed=seed, t=t, err=e), flush=True)
+            print("FAIL", dict(mode=mode, variant=variant, n=n, k=k, s=s, block_rows=br, sms=sms, seed=seed, t=t, err=e),
+                  flush=True)
     print(f"stress_parity: {cases} cases, {fails} failures, {time.time() - t0:.0f} s")
     return 1 if fails else 0
 
