@@ -38,7 +38,12 @@ def main():
         variant = ["cholqr2", "tsqr"][rng.integers(2)]
         s = int(rng.integers(1, 17))
         k = int(rng.integers(0, 120))
-        n = int(rng.integers(max(1000, 2 * (k + s + 16)), 200_000))
+        small = rng.random() < 0.25
+        n = int(rng.integers(k + 3 * s + 2, 4000)) if small else int(rng.integers(max(1000, 2 * (k + s + 16)), 200_000))
+        if rng.random() < 0.2:
+            os.environ["PQR_FORCE_NCCL"] = "1"  # single-rank run through the NCCL exchange path
+        else:
+            os.environ.pop("PQR_FORCE_NCCL", None)
         br = int(rng.choice([0, 0, 512, 768, 1024])) if variant == "tsqr" else 0
         if br and br < 2 * (k + s + 16):
             br = 0
@@ -84,6 +89,16 @@ def main():
                     ok = ok and t == ref["t"] and ei < 1e-10
                     if mode == "append":
                         Qcur = np.asfortranarray(np.hstack([Qcur, ref["U"]]))
+                if mode == "append" and Qcur.shape[1] > 0:
+                    # Y = Q_basis C (the stored basis, explicit or LOR) against the oracle's basis
+                    m = int(rng.integers(1, 9))
+                    C = inputs.gaussian(seed + 99, Qcur.shape[1], m)
+                    Y = torch.empty((m, n), dtype=torch.float64, device="cuda").t()
+                    h.apply(dev(C), m, Y)
+                    torch.cuda.synchronize()
+                    ea = rel(host(Y), Qcur @ C)
+                    e = max(e, ea)
+                    ok = ok and ea < 1e-10
         except Exception as ex:  # noqa: BLE001
             ok, e, t = False, str(ex), None
             if "block plan" in e and br > 512 and s > 8:
@@ -93,7 +108,8 @@ def main():
         cases += 1
         if not ok:
             fails += 1
-            print("FAIL", dict(mode=mode, variant=variant, n=n, k=k, s=s, block_rows=br, sms=sms, seed=seed, t=t, err=e),
+            print("FAIL", dict(mode=mode, variant=variant, n=n, k=k, s=s, block_rows=br, sms=sms,
+                               nccl=os.environ.get("PQR_FORCE_NCCL"), seed=seed, t=t, err=e),
                   flush=True)
     print(f"stress_parity: {cases} cases, {fails} failures, {time.time() - t0:.0f} s")
     return 1 if fails else 0
