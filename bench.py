@@ -368,6 +368,13 @@ def main():
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": traffic, "algorithmic_bytes": per_launch_bytes[dom],
                 "avg_launch_ms": avg_ms}
+    # the same figure for every streaming kernel kind of the step (device events, this run's clocks)
+    roof_all = {}
+    for kd, d in kinds.items():
+        if kd in per_launch_bytes and d["launches"]:
+            am = d["ms"] / d["launches"]
+            roof_all[kd] = {"avg_launch_ms": am, "achieved": per_launch_bytes[kd] / (am * 1e-3) / 1e9,
+                            "frac": per_launch_bytes[kd] / (am * 1e-3) / 1e9 / hbm}
     share = {kd: (d["ms"] / (ms * 1.0)) for kd, d in kinds.items()}
     t_roof = mandatory_bytes(n, k, s) / (hbm * 1e9) * 1e3 * len(variants)
     frac_whole = t_roof / ms_step
@@ -461,6 +468,7 @@ def main():
                        "t": t_vals},
             "frac_of_roofline": frac_whole,
             "roofline": roof,
+            "roofline_by_kernel": roof_all,
             "kernel_share": share,
             "variant_ms_per_call": {v: var_ms[v] / args.steps for v in variants},
             "cpu_baseline": cpu,
