@@ -49,3 +49,22 @@ def test_gpu_arm_json_line():
     assert d["config"]["t"] == [4, 4]
     assert "sm_mhz" in d["clocks"]
 
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """Launched as the driver does for N > 1 (torchrun, 127.0.0.1): rank 0 alone runs the
+    reference arm and prints one JSON line; the other rank exits 0 without work."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--workload", "tiny", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0
