@@ -305,9 +305,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       const int w = pans[UP ? p : np - 1 - p].y;
       const int mtn = (w + 7) >> 3;
       double zp[NT][MTM][2];
-      if constexpr (MTM == 1 && !UP) {
-        // 8-wide panels, stage 2 (measured: slower in stage 1, whose kernel carries the
-        // Householder tail): each warp forms its partial of Z^T = x^T V (A = x from registers,
+      if constexpr (MTM == 1) {
+        // 8-wide panels (stage 1 too since the two-group kernels: 6.65 -> 6.37 ms; with one
+        // 16-warp group it was slower there): each warp forms its partial of Z^T = x^T V (A = x from registers,
         // B = V from the slot) and multiplies it by T (stage 1) or T^T (stage 2) right away, so
         // the summed partials are Z'^T itself; after the barriers a lane only loads the two
         // coefficients it needs (no per-warp MMA chain between the second barrier and the update)
