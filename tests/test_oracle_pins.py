@@ -294,3 +294,74 @@ def test_table1a_magnitudes(orc):
     assert 1e-12 < err["pip"] < 1e-6, err
     assert err["pip+"] < 1e-13, err
     assert err["hh"] < 1e-13, err
+
+
+# ---------------------------------------------------------------------------
+# the deflation branch in the middle of a block (a column deflates, later columns
+# still pivot): orc_cholesky_deflate, orc_update with non-identity pivots and
+# orc_bcgs_pip_plus with t1 < s.  Pins: N^T N = S on every column (the
+# defining identity of the row-echelon N of P:L119), LAPACK Cholesky of S on the
+# pivot columns (uniqueness with positive pivots), numpy solves, Q^T X.
+# ---------------------------------------------------------------------------
+def _dup_middle(n=900, k=7, s=8, seed=31):
+    Q = inputs.orthonormal(seed, n, k)
+    X = inputs.gaussian(seed + 1, n, s)
+    X[:, 5] = X[:, 1]  # column 5 duplicates column 1: in-order deflation drops column 5 only
+    return Q, X
+
+
+def test_cholesky_deflate_mid_block(orc):
+    Q, X = _dup_middle()
+    k, s = Q.shape[1], X.shape[1]
+    W = np.hstack([Q, X]).T @ X
+    S = W[k:] - W[:k].T @ W[:k]
+    nx2 = float(np.linalg.norm(X)) ** 2
+    N, t, piv = orc.cholesky_deflate(W, k=k, tau_abs2=(1e-12) ** 2 * nx2, eta_rel=1e-13)
+    J = [0, 1, 2, 3, 4, 6, 7]
+    assert t == 7 and piv == J
+    # row echelon: row i is zero left of its pivot column, pivots positive, rows >= t zero
+    for i, pc in enumerate(piv):
+        assert np.all(N[i, :pc] == 0) and N[i, pc] > 0
+    assert np.all(N[t:] == 0)
+    # the deflated column is the duplicate's column
+    assert np.allclose(N[:, 5], N[:, 1], rtol=0, atol=1e-12 * np.abs(N).max())
+    # N^T N = S on all columns (including the deflated one)
+    assert rel(N.T @ N, S) < 1e-13
+    # N_J = chol(S_JJ)^T (LAPACK), the pivot-column submatrix
+    assert rel(N[:t][:, J], np.linalg.cholesky(S[np.ix_(J, J)]).T) < 1e-12
+
+
+def test_update_nonidentity_pivots(orc):
+    Q, X = _dup_middle()
+    k = Q.shape[1]
+    P = Q.T @ X
+    J = [0, 1, 2, 3, 4, 6, 7]
+    S = X.T @ X - P.T @ P
+    NJ = np.linalg.cholesky(S[np.ix_(J, J)]).T  # t x t on the pivot columns
+    N = np.zeros((8, 8))
+    N[:7] = np.linalg.solve(NJ.T, S[J])  # full row-echelon N (N_J^T N = S[J, :])
+    U = orc.update(Q, X, P, N, 7, J)
+    want = np.linalg.solve(NJ.T, (X - Q @ P)[:, J].T).T
+    assert rel(U, want) < 1e-12
+    assert np.linalg.norm(np.eye(7) - U.T @ U) < 1e-10 and np.linalg.norm(Q.T @ U) < 1e-12
+    assert k == 7
+
+
+def test_bcgs_pip_plus_deflating(orc):
+    Q, X = _dup_middle()
+    s = X.shape[1]
+    nx2 = float(np.linalg.norm(X)) ** 2
+    out = orc.bcgs_pip_plus(Q, X, tau_abs2=(1e-12) ** 2 * nx2, eta_rel=1e-13)
+    t = out["t"]
+    assert t == s - 1 and out["piv"] == [0, 1, 2, 3, 4, 6, 7]
+    assert rel(out["P"], Q.T @ X) < 1e-13
+    assert residual(Q, X, out["U"], out["P"], out["N"]) < 1e-14
+    assert np.linalg.norm(Q.T @ out["U"], 2) < 1e-13
+    assert np.linalg.norm(np.eye(t) - out["U"].T @ out["U"], 2) < 1e-13
+    N = out["N"]
+    for i, pc in enumerate(out["piv"]):
+        assert np.all(N[i, :pc] == 0) and N[i, pc] > 0
+    assert np.all(N[t:] == 0)
+    # agrees with the Householder oracle (the same in-order deflation, reading R3)
+    hh = orc.householder_pqr(Q, X)
+    assert hh["t"] == t and rel(out["N"], hh["N"]) < 1e-10 and rel(out["U"], hh["U"]) < 1e-10
