@@ -408,6 +408,7 @@ def main():
 
             def worker(v):
                 try:
+                    torch.cuda.set_device(local_rank)  # a new host thread starts on device 0
                     for _ in range(steps):
                         solve_host(v)
                 except Exception as e:  # pragma: no cover

@@ -76,6 +76,10 @@ typedef struct {
   void* stream;         /* cudaStream_t to order all work on; NULL = legacy default stream */
   int rank, nranks;     /* this process's rank and the number of ranks (nranks >= 1)       */
   const void* nccl_id;  /* 128-byte ncclUniqueId (same bytes on all ranks); NULL if nranks==1 */
+  void* vgroup;         /* virtual-rank group (pqr_vgroup_create) or NULL.  When set, the
+                           nranks handles of this group live in ONE process on one device
+                           and exchange through device copies instead of NCCL (see
+                           pqr_vgroup_create); nccl_id is then ignored.                     */
 } pqr_config;
 
 /* Create a handle owning the basis (capacity k_max + s_max columns), its workspaces
@@ -147,6 +151,19 @@ int pqr_get_profile(pqr_handle h, pqr_profile* out);
 
 /* ncclGetUniqueId into a 128-byte buffer (rank 0 creates it; the caller broadcasts it). */
 int pqr_nccl_unique_id(void* id128);
+
+/* Virtual ranks: a group of nranks handles in ONE process on one device that exchange their
+ * small matrices (the (k+s) x s Grams of CholQR2, the (C+s) x s GPU-root blocks of TSQR;
+ * PAPER.md:L1130-1166, §5.2) through device-to-device copies ordered by CUDA events, in
+ * place of ncclAllGather.  Every handle of the group (pqr_config.vgroup = group, rank =
+ * 0..nranks-1) must be created and then driven collectively, each from its own host thread
+ * and with its own stream, exactly as the ranks of a multi-GPU job; results are those of an
+ * nranks-GPU run on the same row shards (bitwise: P, N, t are identical on every rank).  A
+ * rank that stops calling makes its peers' next exchange fail with PQR_ENCCL after 300 s.
+ * The caller owns the group: destroy it after every handle of the group.
+ * Errors: PQR_EARG (nranks < 1 or out NULL). */
+int pqr_vgroup_create(int nranks, void** group);
+int pqr_vgroup_destroy(void* group);
 
 #ifdef __cplusplus
 }

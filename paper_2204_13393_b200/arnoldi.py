@@ -7,19 +7,22 @@ BASELINE configs[2] (7-point Laplacian on a 256^3 grid, s = 4, 32 block iteratio
         [V X] = [V V_{i+1}] [I P; 0 N]  (pqr_project_normalize, appending V_{i+1})
         H_{i+1} = [H_i P; 0 N]
 
-Every step runs in libpqr kernels; this module only sequences the calls and assembles the
-(small, host) block-Hessenberg H.
+Every step runs in libpqr kernels on the device; this module only sequences the calls.  The
+block-Hessenberg H lives on the device: each call writes its P and N straight into their
+slices of H (column offset = the columns of H filled so far, row offset = the basis width),
+so the loop moves no matrix data to the host — the one host value per call is the rank t
+that pqr_project_normalize returns.
 """
 from __future__ import annotations
 
-import numpy as np
-
 
 def block_arnoldi(nx, ny, nz, R, steps, variant="cholqr2", device="cuda", stream=None, timer=None, profile=False):
-    """Run Alg. 1.  R: n x s column-major device tensor.  Returns dict(H, k, t_list, handle_stats,
-    V_last) and keeps the basis in the handle (returned open as 'h' for further queries).
+    """Run Alg. 1.  R: n x s column-major device tensor.  Returns dict(H, H_dev, H0, k, t_list,
+    h, V_last): H_dev is the k x (columns filled) block-Hessenberg matrix on the device (H a
+    host copy taken after the loop), the basis stays in the handle `h` (returned open).
 
     `timer`, if given, is called as timer('pqr'|'op', fn) to time each library call."""
+    import numpy as np
     import torch
 
     from . import inputs, pqr
@@ -31,26 +34,27 @@ def block_arnoldi(nx, ny, nz, R, steps, variant="cholqr2", device="cuda", stream
         h.profile(True)
     run = timer or (lambda kind, fn: fn())
     U = inputs.colmajor_empty(n, s, device)
-    Nb = inputs.colmajor_empty(s, s, device)
-    Pb = inputs.colmajor_empty(max(1, steps * s), s, device)
     X = inputs.colmajor_empty(n, s, device)
-    t0 = run("pqr", lambda: h.solve(R, U=U, N=Nb))
-    H0 = Nb.cpu().numpy()[:t0]
-    H = np.zeros(((steps + 1) * s, steps * s))
+    H0 = inputs.colmajor_empty(s, s, device)
+    Hd = inputs.colmajor_empty((steps + 1) * s, max(1, steps * s), device)
+    Hd.zero_()
+    t0 = run("pqr", lambda: h.solve(R, U=U, N=H0))
     k = t0
+    c0 = 0          # columns of H filled so far (a deflated step adds width < s columns)
     t_list = [t0]
     width = t0
-    for i in range(steps):
+    for _ in range(steps):
         if width == 0:
             break
         run("op", lambda: pqr.pqr_laplacian7_apply(nx, ny, nz, width, U[:, :width], X[:, :width], stream=stream))
-        Pk = Pb[:k] if k > 0 else None
-        t = run("pqr", lambda: h.solve(X[:, :width], U=U, P=Pk, N=Nb, s=width))
-        if k > 0:
-            H[:k, i * s:i * s + width] = Pb[:k].cpu().numpy()[:, :width]
-        H[k:k + t, i * s:i * s + width] = Nb.cpu().numpy()[:t, :width]
+        Pk = Hd[:k, c0:c0 + width] if k > 0 else None
+        Nk = Hd[k:k + width, c0:c0 + width]
+        t = run("pqr", lambda: h.solve(X[:, :width], U=U, P=Pk, N=Nk, s=width))
+        c0 += width
         k += t
         t_list.append(t)
         width = t
     torch.cuda.synchronize()
-    return dict(H=H[:k, :sum(t_list[:-1])], H0=H0, k=k, t_list=t_list, h=h, V_last=U)
+    H_dev = Hd[:k, :c0]
+    return dict(H=np.asfortranarray(H_dev.cpu().numpy()), H_dev=H_dev, H0=H0[:t0].cpu().numpy(), k=k,
+                t_list=t_list, h=h, V_last=U)

@@ -18,6 +18,7 @@
 #include "tsqr_wy.cuh"
 #include "stream_kernels.cuh"
 #include "support_kernels.cuh"
+#include "exchange.cuh"
 
 using namespace pqr;
 
@@ -93,7 +94,8 @@ struct Ctx {
   cudaStream_t cstream = nullptr;  // copy stream of the host-buffer pipeline (created on first use)
   cudaEvent_t hp_in[kHostChunksMax] = {}, hp_out[kHostChunksMax] = {}, hp_done = nullptr;
   double* Wchunks = nullptr;       // kHostChunksMax x (cap x s_max): per-chunk Grams of the first pass
-  ncclComm_t comm = nullptr;
+  Exchange* xc = nullptr;          // cross-rank exchange (nranks > 1, PQR_FORCE_NCCL or a virtual group)
+  int device = 0;                  // the handle's CUDA device (made current at every entry point)
   pqr_stats st{};
   TsqrState* ts = nullptr;
   // profiling (pqr_profile_enable)
@@ -159,6 +161,23 @@ bool is_host_ptr(const void* p) {
   }
   return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
 }
+
+// makes the handle's device current for the duration of a C-ABI call (a handle may be driven
+// from any host thread; a new thread starts on device 0) and restores the caller's device
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -503,9 +522,9 @@ int gram_and_exchange(Ctx* h, int k, int s, const double* Q, const double* X, in
 
 // (nranks > 1) allgather this rank's Gram so every rank sums all ranks' in rank order
 int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts) {
-  if (h->comm) {
+  if (h->xc) {
     PROF(h, PQR_K_NCCL);
-    NCCL_TRY(ncclAllGather(h->Wloc, h->Wall, (size_t)m * s, ncclDouble, h->comm, h->stream));
+    TRY(h->xc->allgather(h->Wloc, h->Wall, (size_t)m * s, h->stream));
     h->st.collectives += 1;
     h->st.collective_bytes += (int64_t)m * s * 8;
     *Wsum = h->Wall;
@@ -654,7 +673,7 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   if (cfg->k_max + cfg->s_max > kMMax) return PQR_ECAPACITY;
   if (cfg->variant != PQR_CHOLQR2 && cfg->variant != PQR_TSQR) return PQR_EARG;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return PQR_EARG;
-  if (cfg->nranks > 1 && !cfg->nccl_id) return PQR_EARG;
+  if (cfg->nranks > 1 && !cfg->nccl_id && !cfg->vgroup) return PQR_EARG;
   if (k > 0 && (!Q || ldq < cfg->n_local)) return PQR_EARG;
   if (k > cfg->n_local) return PQR_EARG;
 
@@ -662,7 +681,8 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   h->cfg = *cfg;
   h->stream = (cudaStream_t)cfg->stream;
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaGetDevice(&dev);  // the caller's current device becomes the handle's device
+  h->device = dev;
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* e = getenv("PQR_SMS")) {  // testing aid: size grids for fewer SMs (several blocks per CTA)
     const int v = atoi(e);
@@ -695,20 +715,31 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   if (cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
   if (cudaMemsetAsync(h->ints, 0, 64 * sizeof(int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
 
-  // PQR_FORCE_NCCL=1 (test aid): a single-rank handle still builds its communicator and runs
-  // every cross-GPU step (allgathers, the replicated cross-GPU tree node) with one rank.
+  // cross-rank exchange: a virtual group (P handles in this process), or NCCL (nranks > 1;
+  // PQR_FORCE_NCCL=1, a test aid, builds a single-rank communicator and runs every cross-GPU
+  // step with one rank)
   static const bool force_nccl = getenv("PQR_FORCE_NCCL") && atoi(getenv("PQR_FORCE_NCCL")) != 0;
-  if (cfg->nranks > 1 || force_nccl) {
+  if (cfg->vgroup) {
+    VirtualGroup* g = reinterpret_cast<VirtualGroup*>(cfg->vgroup);
+    if (g->P != cfg->nranks) return fail(PQR_EARG);
+    auto* vx = new VirtualExchange();
+    h->xc = vx;
+    if (vx->init(g, cfg->rank)) return fail(PQR_ECUDA);
+  } else if (cfg->nranks > 1 || force_nccl) {
     ncclUniqueId id;
     if (cfg->nccl_id) {
       memcpy(&id, cfg->nccl_id, sizeof(id));
     } else if (ncclGetUniqueId(&id) != ncclSuccess) {
       return fail(PQR_ENCCL);
     }
-    ncclResult_t r = ncclCommInitRank(&h->comm, cfg->nranks, id, cfg->rank);
+    auto* nx = new NcclExchange();
+    nx->rank = cfg->rank;
+    nx->nranks = cfg->nranks;
+    h->xc = nx;
+    ncclResult_t r = ncclCommInitRank(&nx->comm, cfg->nranks, id, cfg->rank);
     if (r != ncclSuccess) {
       fprintf(stderr, "[pqr] ncclCommInitRank: %s\n", ncclGetErrorString(r));
-      h->comm = nullptr;
+      nx->comm = nullptr;
       return fail(PQR_ENCCL);
     }
   }
@@ -759,6 +790,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
                           int64_t ldu, double* P, int ldp, double* N, int ldn, int* t) {
   Ctx* h = reinterpret_cast<Ctx*>(hh);
   if (!h || !X || !t || s < 1) return PQR_EARG;
+  DevGuard dg(h->device);
   const int64_t n = h->cfg.n_local;
   const int k = h->k;
   if (s > h->cfg.s_max || k + s > h->cap) return PQR_ECAPACITY;
@@ -777,7 +809,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   h->hp.nch = 0;
   if (x_host) {
     if (!h->stageX && dalloc(&h->stageX, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
-    if (u_host && !h->comm && !(flags & PQR_SINGLE_PASS)) {
+    if (u_host && !h->xc && !(flags & PQR_SINGLE_PASS)) {
       if (h->cfg.variant == PQR_CHOLQR2) {
         if (!h->Wchunks && dalloc(&h->Wchunks, (size_t)kHostChunksMax * h->cap * h->cfg.s_max)) return PQR_ENOMEM;
         TRY(hp_plan_upload(h, X, ldx, s, U, ldu, nullptr));
@@ -849,6 +881,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
 int pqr_basis_apply(pqr_handle hh, const double* C, int ldc, int m, double* Y, int64_t ldy) {
   Ctx* h = reinterpret_cast<Ctx*>(hh);
   if (!h || m < 0 || !Y) return PQR_EARG;
+  DevGuard dg(h->device);
   const int64_t n = h->cfg.n_local;
   const int k = h->k;
   if (ldy < n || (k > 0 && (!C || ldc < k))) return PQR_EARG;
@@ -885,6 +918,7 @@ int pqr_basis_apply(pqr_handle hh, const double* C, int ldc, int m, double* Y, i
 int pqr_destroy(pqr_handle hh) {
   Ctx* h = reinterpret_cast<Ctx*>(hh);
   if (!h) return PQR_OK;
+  DevGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   else cudaDeviceSynchronize();
   tsqr_free(h);
@@ -908,7 +942,7 @@ int pqr_destroy(pqr_handle hh) {
     cudaEventDestroy(h->hp_done);
     cudaStreamDestroy(h->cstream);
   }
-  if (h->comm) ncclCommDestroy(h->comm);
+  delete h->xc;
   for (auto& p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   delete h;
@@ -925,6 +959,7 @@ int pqr_get_stats(pqr_handle hh, pqr_stats* st) {
 int pqr_profile_enable(pqr_handle hh, int enable) {
   Ctx* h = reinterpret_cast<Ctx*>(hh);
   if (!h) return PQR_EARG;
+  DevGuard dg(h->device);
   cudaStreamSynchronize(h->stream);
   prof_collect(h);
   h->prof = enable != 0;
@@ -935,9 +970,21 @@ int pqr_profile_enable(pqr_handle hh, int enable) {
 int pqr_get_profile(pqr_handle hh, pqr_profile* out) {
   Ctx* h = reinterpret_cast<Ctx*>(hh);
   if (!h || !out) return PQR_EARG;
+  DevGuard dg(h->device);
   cudaStreamSynchronize(h->stream);
   prof_collect(h);
   *out = h->prof_tot;
+  return PQR_OK;
+}
+
+int pqr_vgroup_create(int nranks, void** out) {
+  if (!out || nranks < 1 || nranks > 1024) return PQR_EARG;
+  *out = new VirtualGroup(nranks);
+  return PQR_OK;
+}
+
+int pqr_vgroup_destroy(void* group) {
+  delete reinterpret_cast<VirtualGroup*>(group);
   return PQR_OK;
 }
 

@@ -4,10 +4,10 @@
 // Levels (kernels in tsqr_wy.cuh): leaves (level 0) partition the GPU's n_local rows
 // into p0 blocks of ~n_b rows (even starts); each node level stacks `arity` children's
 // top-cap coordinates (R = arity*cap rows per node); the level with one node is the GPU
-// root.  With nranks > 1 the roots' outputs are all-gathered and one more node (the
-// cross-GPU level, arity = nranks, replicated on every GPU) reduces them — the
-// "different algorithm at the cross-GPU level" slot of the paper's framework is this
-// replicated stateful node (§8(e)).  Reflectors are kept in
+// root.  With nranks > 1 the roots' (C+s) x s outputs are all-gathered and the cross-GPU
+// levels — the same arity-bounded tree over the nranks roots, replicated on every GPU —
+// reduce them: the "different algorithm at the cross-GPU level" slot of the paper's
+// framework is this replicated stateful tree (§8(e)).  Reflectors are kept in
 // panels (one per call / per LOR-build chunk) with their compact-WY T factors.
 namespace {
 
@@ -28,13 +28,13 @@ struct TsqrLv {
 struct TsqrState {
   int nb = 0, cap = 0, C = 0, nlev = 0, arity = 8, wmax = 8;
   std::vector<TsqrLv> lv;    // [0] leaves, [1..nlev] nodes
-  TsqrLv xl;                 // cross-GPU node
+  std::vector<TsqrLv> xlv;   // cross-GPU levels ([0] stacks the nranks GPU roots), replicated
   std::vector<int4> panels;  // committed panels (start, width, T offset, merged)
   int4* d_pan = nullptr;     // device copy (+ one uncommitted slot)
   int4* d_panm = nullptr;    // down-sweep list of a merging call
   int merge = 0, mtoff = 0;  // the last call merged its panel into the previous one
   double* in_top = nullptr;  // cap x wmax: GPU root stage-1 output (ld cap)
-  double* xraw = nullptr;    // nranks * cap * wmax allgather receive
+  double* xraw = nullptr;    // nranks * cap * wmax allgather receive (compact (C+s) x s blocks)
   double* Btop = nullptr;    // cap x wmax top coefficients of X (ld cap)
   double* Ut = nullptr;      // cap x wmax top coefficients of U (ld cap)
   double* Rt = nullptr;      // cap x cap explicit top basis (ld cap), zero-init
@@ -149,6 +149,7 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   if (nrun >= 0) { L.b0 = b0; L.nrun = nrun; }
   if (L.nrun == 0) return PQR_OK;
   L.X = X; L.ldx = ldx; L.out = out; L.ldo = ldo;
+  L.orows = ldo < ts->cap ? (int)ldo : ts->cap;  // compact GPU-root block: C + s rows
   L.ovec = ((ts->cap & 1) == 0 && (ldo & 1) == 0 && aligned16(out)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
@@ -204,8 +205,10 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
   const int np = (int)ts->panels.size();
   {
     PROF(h, PQR_K_TSQR_LOCAL);
+    // the GPU root's block goes compact ((C+s) x s, ld C+s) when it is all-gathered
+    const int64_t ldtop = h->xc ? C + s : ts->cap;
     double* out0 = ts->nlev >= 1 ? ts->lv[1].in : ts->in_top;
-    const int64_t ldo0 = ts->nlev >= 1 ? ts->lv[1].rows : ts->cap;
+    const int64_t ldo0 = ts->nlev >= 1 ? ts->lv[1].rows : ldtop;
     if (pipe && h->hp.nch > 0) {
       // host X arrives chunk by chunk (leaf blocks are independent in stage 1)
       for (int c = 0; c < h->hp.nch; ++c) {
@@ -218,26 +221,34 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
   }
   {
     PROF(h, PQR_K_TSQR_TREE);
+    const int64_t ldtop = h->xc ? C + s : ts->cap;
     for (int l = 1; l <= ts->nlev; ++l) {
       const bool root = l == ts->nlev;
       TRY(run_wy_up(h, ts->lv[l], ts->lv[l].in, ts->lv[l].rows, root ? ts->in_top : ts->lv[l + 1].in,
-                    root ? ts->cap : ts->lv[l + 1].rows, np, C, s, merge, mtoff));
+                    root ? ldtop : ts->lv[l + 1].rows, np, C, s, merge, mtoff));
     }
   }
-  if (h->comm) {
+  if (h->xc) {
     const int P = h->cfg.nranks;
+    const size_t cnt = (size_t)(C + s) * s;
     {
       PROF(h, PQR_K_NCCL);
-      NCCL_TRY(ncclAllGather(ts->in_top, ts->xraw, (size_t)ts->cap * s, ncclDouble, h->comm, h->stream));
+      TRY(h->xc->allgather(ts->in_top, ts->xraw, cnt, h->stream));
       h->st.collectives += 1;
-      h->st.collective_bytes += (int64_t)ts->cap * s * 8;
+      h->st.collective_bytes += (int64_t)cnt * 8;
     }
     PROF(h, PQR_K_TSQR_TREE);
-    for (int g = 0; g < P; ++g)
-      CUDA_TRY(cudaMemcpy2DAsync(ts->xl.in + (int64_t)g * ts->cap, (size_t)ts->xl.rows * sizeof(double),
-                                 ts->xraw + (int64_t)g * ts->cap * s, (size_t)ts->cap * sizeof(double),
-                                 (size_t)ts->cap * sizeof(double), s, cudaMemcpyDeviceToDevice, h->stream));
-    TRY(run_wy_up(h, ts->xl, ts->xl.in, ts->xl.rows, ts->Btop, ts->cap, np, C, s, merge, mtoff));
+    TsqrLv& x0 = ts->xlv[0];
+    k_unpack_roots<<<std::max(1, std::min(64, (int)(((size_t)P * ts->cap * s + 255) / 256))), 256, 0, h->stream>>>(
+        ts->xraw, C + s, s, P, x0.in, x0.rows, ts->cap);
+    ++h->st.kernel_launches;
+    CUDA_TRY(cudaGetLastError());
+    const int nx = (int)ts->xlv.size();
+    for (int l = 0; l < nx; ++l) {
+      const bool top = l == nx - 1;
+      TRY(run_wy_up(h, ts->xlv[l], ts->xlv[l].in, ts->xlv[l].rows, top ? ts->Btop : ts->xlv[l + 1].in,
+                    top ? ts->cap : ts->xlv[l + 1].rows, np, C, s, merge, mtoff));
+    }
   }
   return PQR_OK;
 }
@@ -251,10 +262,17 @@ int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol
   int64_t root_ld = ts->cap;
   {
     PROF(h, PQR_K_TSQR_TREE);
-    if (h->comm) {
-      TRY(run_wy_down(h, ts->xl, cin, ts->cap, ts->xl.dn, ts->xl.rows, np, Call, t, ncol, pan));
-      root_cin = ts->xl.dn + (int64_t)h->cfg.rank * ts->cap;
-      root_ld = ts->xl.rows;
+    if (h->xc) {
+      // the replicated cross-GPU levels, top down; this rank's root is child `rank` of the
+      // first cross level
+      const int nx = (int)ts->xlv.size();
+      for (int l = nx - 1; l >= 0; --l) {
+        const bool top = l == nx - 1;
+        TRY(run_wy_down(h, ts->xlv[l], top ? cin : ts->xlv[l + 1].dn, top ? ts->cap : ts->xlv[l + 1].rows,
+                        ts->xlv[l].dn, ts->xlv[l].rows, np, Call, t, ncol, pan));
+      }
+      root_cin = ts->xlv[0].dn + (int64_t)h->cfg.rank * ts->cap;
+      root_ld = ts->xlv[0].rows;
     }
     for (int l = ts->nlev; l >= 1; --l) {
       const bool root = l == ts->nlev;
@@ -400,14 +418,32 @@ int tsqr_alloc(Ctx* h) {
   CUDA_TRY(cudaMemsetAsync(ts->Rt, 0, sizeof(double) * cap * cap, h->stream));
   if ((rc = dalloc(&ts->coef, (size_t)cap * 16))) return rc;
   if ((rc = dalloc(&ts->d_pan, (size_t)cap + 1)) || (rc = dalloc(&ts->d_panm, (size_t)cap + 1))) return rc;
-  if (h->comm) {
-    TsqrLv& x = ts->xl;
-    x.nblocks = 1;
-    x.q = (int64_t)h->cfg.nranks * cap;
-    x.rows = x.q + (x.q & 1);
-    x.ldv = x.rows;
-    TRY(alloc_level(h, x, wmax, true));
-    if ((rc = dalloc(&ts->xraw, (size_t)x.rows * wmax))) return rc;
+  if (h->xc) {
+    // cross-GPU levels over the nranks GPU roots, arity-bounded like the on-GPU node levels
+    // (a level with more children than the arity is split into nodes of arity children; the
+    // last level is one node of its children, an odd row count kept as the odd last row)
+    int cnt = h->cfg.nranks;
+    ts->xlv.clear();
+    for (;;) {
+      TsqrLv x;
+      if (cnt <= ts->arity) {
+        const int64_t r = (int64_t)cnt * cap;
+        x.nblocks = 1;
+        x.q = r & ~int64_t(1);
+        x.odd_last = (int)(r & 1);
+        x.rows = r + (r & 1);
+      } else {
+        x.nblocks = (cnt + ts->arity - 1) / ts->arity;
+        x.q = (int64_t)ts->arity * cap;
+        x.rows = (int64_t)x.nblocks * x.q;
+      }
+      x.ldv = x.rows;
+      TRY(alloc_level(h, x, wmax, true));
+      ts->xlv.push_back(x);
+      if (x.nblocks == 1) break;
+      cnt = x.nblocks;
+    }
+    if ((rc = dalloc(&ts->xraw, (size_t)h->cfg.nranks * cap * wmax))) return rc;
     if ((rc = dalloc(&ts->Btop, (size_t)cap * wmax))) return rc;
   } else {
     ts->Btop = ts->in_top;
@@ -558,7 +594,7 @@ void tsqr_free(Ctx* h) {
   TsqrState* ts = h->ts;
   if (!ts) return;
   for (auto& lv : ts->lv) free_level(lv);
-  free_level(ts->xl);
+  for (auto& lv : ts->xlv) free_level(lv);
   cudaFree(ts->in_top);
   cudaFree(ts->xraw);
   if (ts->Btop != ts->in_top) cudaFree(ts->Btop);

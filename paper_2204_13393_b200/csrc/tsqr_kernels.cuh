@@ -190,4 +190,17 @@ __global__ void __launch_bounds__(256) k_tsqr_top(TsqrTopArgs a) {
   }
 }
 
+// Cross-GPU level input (a7, §8(e)): the all-gathered GPU-root blocks, rank-major and compact
+// (block g = rows x s with ld rows at src + g*rows*s), into the first cross level's stacked
+// input: block g at rows g*cap of dst (ld ldd); rows rows..cap-1 of each child slot are
+// zeroed (an earlier call with a wider block may have left data there).
+__global__ void __launch_bounds__(256) k_unpack_roots(const double* __restrict__ src, int rows, int s, int P,
+                                                      double* __restrict__ dst, int64_t ldd, int cap) {
+  const int per = cap * s;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < P * per; e += gridDim.x * blockDim.x) {
+    const int g = e / per, r = e - g * per, c = r / cap, i = r - c * cap;
+    dst[(int64_t)g * cap + i + (int64_t)c * ldd] = i < rows ? src[(int64_t)g * rows * s + c * rows + i] : 0.0;
+  }
+}
+
 }  // namespace pqr

@@ -64,6 +64,8 @@ struct WyLevel {
                                     // and row R of an odd-sized last block is a zero pad row
   double* T; int64_t tstride;       // block b's T area at T + b*tstride; panel at +16*start
   double* out; int64_t ldo;         // stage-1 output: block b -> rows b*cap ...
+  int orows;                        // ... rows written per block: min(R, orows) (cap, or C+s for a
+                                    // compact GPU-root block that is all-gathered)
   int ovec;                         // out 16-B aligned with even cap and ldo (paired stores)
   const double* cin; int64_t ldci;  // stage-2 coefficients: block b -> rows b*cap ...
   double* Y; int64_t ldy;           // stage-2 output (level rows)
@@ -830,7 +832,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     // so a warp writes each column as one contiguous 16-byte-per-lane store.
     {
       double* outb = L.out + b * L.cap;
-      const int rmax = R < L.cap ? R : L.cap;
+      const int rmax = R < L.orows ? R : L.orows;
 #pragma unroll
       for (int c = 0; c < S8; ++c) {
         if (c >= s) break;

@@ -34,7 +34,7 @@ class pqr_config(ctypes.Structure):
         ("n_local", ctypes.c_int64), ("k_max", ctypes.c_int), ("s_max", ctypes.c_int),
         ("variant", ctypes.c_int), ("defl_tol", ctypes.c_double), ("gram_eta", ctypes.c_double),
         ("block_rows", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
-        ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+        ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("vgroup", ctypes.c_void_p),
     ]
 
 
@@ -54,6 +54,7 @@ PROFILE_KINDS = ["gram", "factor", "update", "nccl", "tsqr_local", "tsqr_tree", 
 
 EXPORTS = ["pqr_create", "pqr_project_normalize", "pqr_basis_apply", "pqr_destroy", "pqr_strerror",
            "pqr_get_stats", "pqr_profile_enable", "pqr_get_profile", "pqr_nccl_unique_id",
+           "pqr_vgroup_create", "pqr_vgroup_destroy",
            "pqr_step_gram", "pqr_step_factor", "pqr_step_update", "pqr_laplacian7_apply"]
 
 _lib = None
@@ -78,6 +79,8 @@ def lib():
     L.pqr_profile_enable.argtypes = [vp, i]
     L.pqr_get_profile.argtypes = [vp, ctypes.POINTER(pqr_profile)]
     L.pqr_nccl_unique_id.argtypes = [vp]
+    L.pqr_vgroup_create.argtypes = [i, ctypes.POINTER(vp)]
+    L.pqr_vgroup_destroy.argtypes = [vp]
     L.pqr_step_gram.argtypes = [i64, i, i, vp, i64, vp, i64, vp, i, vp]
     L.pqr_step_factor.argtypes = [i, i, vp, i, d, d, vp, i, vp, i, ctypes.POINTER(ctypes.c_int),
                                   ctypes.POINTER(ctypes.c_int), vp]
@@ -112,10 +115,12 @@ def _mat(a, rows=None):
         if isinstance(a, torch.Tensor):
             if a.dtype != torch.float64:
                 raise TypeError("pqr: matrices must be float64")
+            # every column must be contiguous (a strided view such as A[:, j] of a row-major
+            # matrix would otherwise be read as contiguous rows)
+            if a.dim() not in (1, 2) or (a.shape[0] > 1 and a.stride(0) != 1):
+                raise ValueError("pqr: matrices must be column-major (stride(0) == 1)")
             if a.dim() == 1:
                 return a.data_ptr(), max(1, a.shape[0])
-            if a.shape[1] > 1 and a.stride(0) != 1:
-                raise ValueError("pqr: matrices must be column-major (stride(0) == 1)")
             ld = a.stride(1) if a.shape[1] > 1 else max(1, a.shape[0])
             return a.data_ptr(), ld
     except ImportError:  # pragma: no cover
@@ -125,10 +130,10 @@ def _mat(a, rows=None):
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64:
             raise TypeError("pqr: matrices must be float64")
+        if a.ndim not in (1, 2) or (a.shape[0] > 1 and a.strides[0] != 8) or (a.ndim == 2 and a.strides[1] % 8):
+            raise ValueError("pqr: matrices must be column-major (contiguous columns)")
         if a.ndim == 1:
             return a.ctypes.data, max(1, a.shape[0])
-        if a.shape[1] > 1 and not a.flags.f_contiguous and a.strides[0] != 8:
-            raise ValueError("pqr: matrices must be column-major")
         ld = a.strides[1] // 8 if a.shape[1] > 1 else max(1, a.shape[0])
         return a.ctypes.data, ld
     if isinstance(a, int):
@@ -150,7 +155,7 @@ def _stream_ptr(stream):
 # C-ABI mirror (same names)
 # ---------------------------------------------------------------------------
 def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0.0, gram_eta=0.0, block_rows=0,
-               stream=None, rank=0, nranks=1, nccl_id: bytes | None = None):
+               stream=None, rank=0, nranks=1, nccl_id: bytes | None = None, vgroup=None):
     cfg = pqr_config()
     cfg.n_local = int(n_local)
     cfg.k_max = int(k_max)
@@ -162,19 +167,46 @@ def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0
     cfg.stream = _stream_ptr(stream)
     cfg.rank = int(rank)
     cfg.nranks = int(nranks)
+    cfg.vgroup = vgroup.value if isinstance(vgroup, ctypes.c_void_p) else vgroup
     idbuf = None
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         cfg.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     qp, ldq = _mat(Q) if (Q is not None and k > 0) else (None, max(1, int(n_local)))
     h = ctypes.c_void_p()
+    if Q is not None and k > 0:
+        _need(Q, int(n_local), int(k), "Q")
     _check(lib().pqr_create(ctypes.byref(h), ctypes.byref(cfg), qp, ldq, int(k)), "pqr_create")
+    _n_local[h.value] = int(n_local)
     return h
+
+
+def _shape(a):
+    if a is None or isinstance(a, int):
+        return None
+    sh = tuple(a.shape)
+    return sh if len(sh) == 2 else (sh[0], 1)
+
+
+def _need(a, rows, cols, what):
+    """Refuse an undersized buffer (the library would read or write past its end)."""
+    sh = _shape(a)
+    if sh is not None and (sh[0] < rows or sh[1] < cols):
+        raise ValueError(f"pqr: {what} has shape {sh}, needs at least ({rows}, {cols})")
+
+
+_n_local = {}  # handle value -> n_local (shape checks of the wrappers)
 
 
 def pqr_project_normalize(h, X, s=None, flags=0, U=None, P=None, N=None):
     xp, ldx = _mat(X)
     s = int(s if s is not None else X.shape[1])
+    n = _n_local.get(h.value if isinstance(h, ctypes.c_void_p) else h, 0)
+    _need(X, n, s, "X")
+    _need(U, n, s, "U")
+    _need(N, s, s, "N")
+    if P is not None:
+        _need(P, pqr_get_stats(h)["k"], s, "P")
     up, ldu = _mat(U)
     pp, ldp = _mat(P)
     np_, ldn = _mat(N)
@@ -185,6 +217,10 @@ def pqr_project_normalize(h, X, s=None, flags=0, U=None, P=None, N=None):
 
 
 def pqr_basis_apply(h, C, m, Y):
+    n = _n_local.get(h.value if isinstance(h, ctypes.c_void_p) else h, 0)
+    _need(Y, n, int(m), "Y")
+    if C is not None:
+        _need(C, pqr_get_stats(h)["k"], int(m), "C")
     cp, ldc = _mat(C)
     yp, ldy = _mat(Y)
     _check(lib().pqr_basis_apply(h, cp, ldc, int(m), yp, ldy), "pqr_basis_apply")
@@ -192,6 +228,7 @@ def pqr_basis_apply(h, C, m, Y):
 
 def pqr_destroy(h):
     if h is not None and h.value:
+        _n_local.pop(h.value, None)
         _check(lib().pqr_destroy(h), "pqr_destroy")
 
 
@@ -215,6 +252,18 @@ def pqr_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().pqr_nccl_unique_id(buf), "pqr_nccl_unique_id")
     return buf.raw
+
+
+def pqr_vgroup_create(nranks):
+    """A group of `nranks` virtual ranks (handles in this process exchanging through device copies)."""
+    g = ctypes.c_void_p()
+    _check(lib().pqr_vgroup_create(int(nranks), ctypes.byref(g)), "pqr_vgroup_create")
+    return g
+
+
+def pqr_vgroup_destroy(g):
+    if g is not None and g.value:
+        _check(lib().pqr_vgroup_destroy(g), "pqr_vgroup_destroy")
 
 
 def pqr_step_gram(n, k, s, Q, X, W, stream=None):

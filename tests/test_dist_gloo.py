@@ -1,6 +1,9 @@
-"""World-size-2 tests of the multi-GPU path's host logic on CPU (gloo): row sharding, the
+"""World-size-2 tests of the multi-GPU path's HOST logic on CPU (gloo): row sharding, the
 NCCL-id broadcast plumbing, the cross-rank Gram reduction (a2) and the TSQR cross-GPU level
-(R12), emulated with the oracle on each rank's shard."""
+(R12).  ORACLE-ONLY: the per-rank arithmetic here is the CPU oracle on each rank's shard; the
+library's own multi-rank code (exchanges, cross-GPU tree, nparts = nranks) is executed by
+tests/test_gpu_vranks.py (virtual ranks on one GPU) and tests/test_gpu_multigpu.py (torchrun
+over >= 2 GPUs, skipped with fewer)."""
 import os
 import socket
 import sys

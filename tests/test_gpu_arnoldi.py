@@ -46,19 +46,27 @@ def lap7_numpy(V, nx, ny, nz):
 
 
 def oracle_arnoldi(orc, R, nx, steps):
+    """Alg. 1 with the oracle's PQR (widths follow the oracle's t: a deflated step adds fewer
+    columns to H, at the running column offset)."""
     n, s = R.shape
     out = orc.householder_pqr(None, R)
     V = out["U"]
     H = np.zeros(((steps + 1) * s, steps * s))
-    k = s
+    k = out["t"]
+    w = k
+    c0 = 0
     for i in range(steps):
-        X = lap7_numpy(V[:, k - s:k], nx, nx, nx)
+        if w == 0:
+            break
+        X = lap7_numpy(V[:, k - w:k], nx, nx, nx)
         o = orc.householder_pqr(V, X)
-        H[:k, i * s:(i + 1) * s] = o["P"]
-        H[k:k + s, i * s:(i + 1) * s] = o["N"]
+        H[:k, c0:c0 + w] = o["P"]
+        H[k:k + o["t"], c0:c0 + w] = o["N"][:o["t"]]
         V = np.hstack([V, o["U"]])
-        k += s
-    return V, H
+        c0 += w
+        k += o["t"]
+        w = o["t"]
+    return V, H[:k, :c0]
 
 
 def test_stencil_vs_numpy(P):
@@ -83,6 +91,33 @@ def test_arnoldi_vs_oracle_small(P, orc, variant):
     assert out["t_list"] == [s] * (steps + 1)
     assert rel(out["H"], H_ref) < 1e-10
     out["h"].close()
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_arnoldi_deflated_start_block(P, orc, variant):
+    """A rank-deficient start block (column 2 = column 0): t = 3 at every step, so H has 3
+    columns per block at the running offset; it must match the oracle's Arnoldi and satisfy
+    A V_m = V_{m+1} H."""
+    import torch
+
+    from paper_2204_13393_b200.arnoldi import block_arnoldi
+
+    nx, s, steps = 10, 4, 5
+    R = inputs.gaussian(7, nx ** 3, s)
+    R[:, 2] = R[:, 0]
+    out = block_arnoldi(nx, nx, nx, dev(R), steps, variant=variant)
+    assert out["t_list"] == [3] * (steps + 1)
+    V_ref, H_ref = oracle_arnoldi(orc, R, nx, steps)
+    assert out["H"].shape == H_ref.shape == (3 * (steps + 1), 3 * steps)
+    assert rel(out["H"], H_ref) < 1e-10
+    h, k = out["h"], out["k"]
+    V = empty(nx ** 3, k)
+    h.apply(dev(np.eye(k)), k, V)
+    torch.cuda.synchronize()
+    Vh = host(V)
+    m = out["H"].shape[1]
+    assert np.linalg.norm(lap7_numpy(Vh[:, :m], nx, nx, nx) - Vh @ out["H"]) < 1e-11 * math.sqrt(m) * 12
+    h.close()
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
