@@ -35,6 +35,8 @@ PQR_DEV void dmma884(double& d0, double& d1, double a, double b) {
 PQR_DEV double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 PQR_DEV double2 ld2_stream(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
 
+PQR_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
 PQR_DEV void st2(double* p, double x, double y) { *reinterpret_cast<double2*>(p) = make_double2(x, y); }
 
 // Column pointer of A = [Q X] (Q: columns 0..k-1, X: columns k..m-1); nullptr past m.
@@ -131,6 +133,14 @@ namespace pqr {
 PQR_DEV void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                : "memory");
+}
+// bulk prefetch of [p, p + bytes) into L2 (bytes % 16 == 0, p 16-B aligned)
+PQR_DEV void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+// as cp_async16 with a 32-bit shared-memory address
+PQR_DEV void cp_async16_s(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 PQR_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>

@@ -17,6 +17,7 @@
 #include "tsqr_kernels.cuh"
 #include "tsqr_wy.cuh"
 #include "stream_kernels.cuh"
+#include "stream2_kernels.cuh"
 #include "support_kernels.cuh"
 #include "exchange.cuh"
 
@@ -320,6 +321,7 @@ cudaError_t launch_gram_mtw(const GramPlan& p, const GramArgs& a, bool vec, cuda
 }
 
 constexpr int kSmemBudget = 225 * 1024;
+int run_s2(int mode, const S2Args& a0, int sms, cudaStream_t st, int64_t* launches);
 
 template <int MTH, int NT, int RB>
 cudaError_t launch_gram_cpa_t(int grid, size_t smem, const GramCpaArgs& a, cudaStream_t st) {
@@ -333,6 +335,14 @@ cudaError_t launch_gram_cpa_t(int grid, size_t smem, const GramCpaArgs& a, cudaS
 int run_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const double* X, int64_t ldx,
              double* W, int ldw, double* partials, unsigned int* ticket, int sms, cudaStream_t st,
              int64_t* launches) {
+  static const bool s2g = getenv("PQR_S2_GRAM") && atoi(getenv("PQR_S2_GRAM")) != 0;
+  if (s2g) {
+    S2Args b{};
+    b.Q = Q; b.ldq = ldq; b.X = X; b.ldx = ldx; b.n = n; b.k = k; b.sx = s; b.sout = 0;
+    b.partials = partials; b.W = W; b.ldw = ldw; b.ticket = ticket;
+    const int rc = run_s2(kS2Gram, b, sms, st, launches);
+    if (rc != PQR_EPLAN) return rc;
+  }
   const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (ldx & 1) == 0 && aligned16(X);
   static const int env_rb = getenv("PQR_GRAM_RB") ? atoi(getenv("PQR_GRAM_RB")) : 32;
   // two CTAs per SM (two stages each) beat one CTA with five stages for wide [Q X] (weak
@@ -390,6 +400,14 @@ int run_update(int64_t n, int k, const double* Q, int64_t ldq, int sx, const dou
                const double* M, int ldm, int sout, const int* t_dev, double* U, int64_t ldu,
                double* U2, int64_t ldu2, int sms, cudaStream_t st, int64_t* launches) {
   if (n <= 0 || sout <= 0) return PQR_OK;
+  static const bool s2u = getenv("PQR_S2_UPD") && atoi(getenv("PQR_S2_UPD")) != 0;
+  if (s2u) {
+    S2Args b{};
+    b.Q = Q; b.ldq = ldq; b.X = X; b.ldx = ldx; b.n = n; b.k = k; b.sx = sx; b.sout = sout;
+    b.M = M; b.ldm = ldm; b.t_dev = t_dev; b.U = U; b.ldu = ldu; b.U2 = U2; b.ldu2 = ldu2;
+    const int rc = run_s2(kS2Update, b, sms, st, launches);
+    if (rc != PQR_EPLAN) return rc;
+  }
   UpdateArgs a{};
   a.Q = Q; a.ldq = ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.sx = sx; a.sout = sout;
   a.M = M; a.ldm = ldm; a.t_dev = t_dev; a.U = U; a.ldu = ldu; a.U2 = U2; a.ldu2 = ldu2;
@@ -455,6 +473,43 @@ int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches) {
   return PQR_OK;
 }
 
+// Producer-free warp-unit streaming kernels (stream2_kernels.cuh).  mode: kS2Fused (default for
+// the fused pass; PQR_S2=0 disables), kS2Gram / kS2Update (PQR_S2_GRAM=1 / PQR_S2_UPD=1).
+// Returns PQR_EPLAN when no instantiation fits (the caller uses the stream_kernels.cuh kernels).
+int run_s2(int mode, const S2Args& a0, int sms, cudaStream_t st, int64_t* launches) {
+  const int MT = (a0.k + a0.sx + 7) / 8;
+  const int NT = (mode == kS2Gram ? a0.sx : a0.sout) > 8 ? 2 : 1;
+  if (MT > 20 || (NT == 2 && MT > 10)) return PQR_EPLAN;  // beyond: register spills
+  const bool vec = (a0.k == 0 || ((a0.ldq & 1) == 0 && aligned16(a0.Q))) &&
+                   (a0.sx == 0 || ((a0.ldx & 1) == 0 && aligned16(a0.X))) &&
+                   (mode == kS2Gram || ((a0.ldu & 1) == 0 && aligned16(a0.U))) &&
+                   (!a0.U2 || ((a0.ldu2 & 1) == 0 && aligned16(a0.U2)));
+  if (!vec) return PQR_EPLAN;
+  S2Args a = a0;
+  a.nslot = s2_nslot(MT, kSmemBudget);
+  // refill copies interleaved with the G phase: faster up to 12 tiles (config S: 2.14 -> 1.95 ms),
+  // slower at 17 (weak config: 7.7 -> 9.3 ms); PQR_S2_IL=0|1 forces
+  static const int env_il = getenv("PQR_S2_IL") ? atoi(getenv("PQR_S2_IL")) : -1;
+  static const int env_pf = getenv("PQR_S2_PF") ? atoi(getenv("PQR_S2_PF")) : 0;
+  static const int env_lp = getenv("PQR_S2_LOOP") ? atoi(getenv("PQR_S2_LOOP")) : 1;
+  a.issue_loop = env_lp;
+  a.interleave = env_il >= 0 ? env_il : (MT <= 12 ? 1 : 0);
+  a.pf_rounds = env_pf;
+  if (a.nslot < kS2Consumers + 1) return PQR_EPLAN;
+  const int64_t nunits = (a.n + kS2Rows - 1) / kS2Rows;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, nunits));
+  cudaError_t e = mode == kS2Fused ? pqr_launch_s2_fused(a, grid, st)
+                  : mode == kS2Gram ? pqr_launch_s2_gram(a, grid, st)
+                                    : pqr_launch_s2_update(a, grid, st);
+  if (e == cudaErrorNotSupported) return PQR_EPLAN;
+  if (launches) ++*launches;
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[pqr] stream2 launch (mode %d): %s\n", mode, cudaGetErrorString(e));
+    return PQR_ECUDA;
+  }
+  return PQR_OK;
+}
+
 // Fused second CholQR pass: U1 = [Q X] M1 (into U1) and W2 = [Q U1]^T U1 (into W).
 // Returns PQR_EPLAN when the fused kernel cannot be used (caller falls back).
 template <int MTH, int NT>
@@ -469,6 +524,15 @@ int run_update_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const
                     const double* M, int ldm, const int* t_dev, double* U1, int64_t ldu, double* W, int ldw,
                     double* partials, unsigned int* ticket, int sms, cudaStream_t st, int64_t* launches) {
   static const bool disabled = getenv("PQR_NO_FUSE") != nullptr;
+  static const bool s2 = !(getenv("PQR_S2") && atoi(getenv("PQR_S2")) == 0);
+  if (!disabled && s2) {
+    S2Args b{};
+    b.Q = Q; b.ldq = ldq; b.X = X; b.ldx = ldx; b.n = n; b.k = k; b.sx = s; b.sout = s;
+    b.M = M; b.ldm = ldm; b.t_dev = t_dev; b.U = U1; b.ldu = ldu;
+    b.partials = partials; b.W = W; b.ldw = ldw; b.ticket = ticket;
+    const int rc = run_s2(kS2Fused, b, sms, st, launches);
+    if (rc != PQR_EPLAN) return rc;
+  }
   const bool vec = (k == 0 || ((ldq & 1) == 0 && aligned16(Q))) && (ldx & 1) == 0 && aligned16(X) &&
                    (ldu & 1) == 0 && aligned16(U1);
   const int m = k + s, MT = (m + 7) / 8, MTH = (MT + 1) / 2, NT = s > 8 ? 2 : 1;

@@ -31,8 +31,6 @@ namespace pqr {
 constexpr int kCpaThreads = 256;
 constexpr int kCpaWarps = kCpaThreads / 32;
 
-PQR_DEV double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
-
 // 16-byte chunk of rows (row, row+1) of a column, zero-filled past n (or for a missing
 // column: colp == nullptr).  `safe` is any valid global address (not read when 0 bytes).
 PQR_DEV void cp_rows(double* dst, const double* colp, int64_t row, int64_t n, const double* safe) {

@@ -1,7 +1,6 @@
 """Build the current sources into build/<name>/libpqr.so with extra nvcc flags (A/B and trace builds;
 the in-tree product library is untouched).  python tools/build_variant.py NAME [-DFOO ...]"""
 import os
-import subprocess
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,8 +9,4 @@ from paper_2204_13393_b200 import build as b  # noqa: E402
 name, extra = sys.argv[1], sys.argv[2:]
 out = os.path.join(b.ROOT, "build", name, "libpqr.so")
 os.makedirs(os.path.dirname(out), exist_ok=True)
-inc, libdir = b.nccl_dirs()
-subprocess.check_call([b.NVCC, *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-                       "-I", inc, "-I", os.path.join(b.ROOT, "include"), *extra, *b.sources(), "-o", out,
-                       "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}", "-lcudart"])
-print(out)
+print(b.build(force=True, defines=extra, out=out))
