@@ -175,6 +175,40 @@ def oracle_sample(w, target_s=15.0, max_rows=None):
     return gbs, info, dt
 
 
+def host_info():
+    """CPU model and core counts of the box (the oracle's machine)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def single_thread_oracle():
+    """The oracle with one OpenMP thread (a subprocess: the thread count is fixed at load) on
+    configs[0] in full and on a 2^18-row sample of configs[1]'s shape."""
+    import subprocess
+
+    code = ("import json,time,sys; sys.path.insert(0, %r)\n"
+            "import oracle\nfrom paper_2204_13393_b200 import inputs\nout = {}\n"
+            "for name, n, k, s in (('tiny', 10000, 32, 4), ('single_sample', 2**18, 64, 8)):\n"
+            "    Q = inputs.orthonormal(7, n, k); X = inputs.gaussian(8, n, s)\n"
+            "    t0 = time.perf_counter(); oracle.householder_pqr(Q, X); dt = time.perf_counter() - t0\n"
+            "    out[name] = {'rows': n, 'k': k, 's': s, 'seconds': dt, 'GB/s': 8.0 * n * (k + 2 * s) / dt / 1e9}\n"
+            "out['threads'] = oracle.num_threads()\nprint(json.dumps(out))\n") % ROOT
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, OMP_NUM_THREADS="1"))
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -376,7 +410,10 @@ def main():
             roof_all[kd] = {"avg_launch_ms": am, "achieved": per_launch_bytes[kd] / (am * 1e-3) / 1e9,
                             "frac": per_launch_bytes[kd] / (am * 1e-3) / 1e9 / hbm}
     share = {kd: (d["ms"] / (ms * 1.0)) for kd, d in kinds.items()}
-    t_roof = mandatory_bytes(n, k, s) / (hbm * 1e9) * 1e3 * len(variants)
+    # north_star roofline: mandatory bytes / HBM + the measured latency of the small exchanges
+    # (device time of the collectives in this run, per step; 0 on one GPU without NCCL)
+    nccl_ms_step = kinds.get("nccl", {}).get("ms", 0.0) / args.steps
+    t_roof = mandatory_bytes(n, k, s) / (hbm * 1e9) * 1e3 * len(variants) + nccl_ms_step
     frac_whole = t_roof / ms_step
 
     # ---- e2e through the C-ABI with HOST buffers (pinned), copies inside the timed region ----
@@ -451,6 +488,8 @@ def main():
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
             _, cpu, _ = oracle_sample(w, target_s=25.0)
+            cpu.update(host_info())
+            cpu["single_thread"] = single_thread_oracle()
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "error": str(e)}
 
@@ -468,6 +507,7 @@ def main():
                        else "inputs fit in L2 (latency-bound config)",
                        "t": t_vals},
             "frac_of_roofline": frac_whole,
+            "roofline_terms_ms": {"hbm": t_roof - nccl_ms_step, "nccl": nccl_ms_step},
             "roofline": roof,
             "roofline_by_kernel": roof_all,
             "kernel_share": share,

@@ -162,35 +162,71 @@ struct FactorArgs {
   double* Pf; int ldpf; double* Nf; int ldnf; int* tf;
 };
 
-__global__ void __launch_bounds__(256) k_factor(FactorArgs a) {
+// The whole factorisation by one CTA (any blockDim; callers use 256).  Output pointers may be
+// global or shared memory (generic addressing): the small-n persistent kernel runs it in every
+// CTA on the same summed Gram, writing to per-CTA shared buffers (identical results).
+#ifdef PQR_SMALL_TRACE
+__device__ unsigned long long g_factor_trace[8];
+#define FB_TR(i)                                                                          \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                                                \
+    unsigned long long t_;                                                                \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+    g_factor_trace[i] = t_;                                                               \
+  }
+#else
+#define FB_TR(i)
+#endif
+__device__ __forceinline__ void factor_body(const FactorArgs& a) {
+  FB_TR(0);
   __shared__ double sW[kMMax * kSMax];
   __shared__ double sS[kSMax * kSMax];
   __shared__ double sN[kSMax * kSMax];
   __shared__ double sNi[kSMax * kSMax];
   __shared__ int sPiv[kSMax];
   __shared__ int sT;
+  __shared__ double sInv[kSMax];  // 1 / N(r, pivot r)
   const int tid = threadIdx.x;
   const int k = a.k;
   const int s = a.s_dev ? min(*a.s_dev, a.s) : a.s;
   const int m = k + s;
 
-  // 1. sum the per-rank Gram matrices in rank order
+  // 1. sum the per-part Gram matrices (ranks, host-buffer chunks, or CTAs) in a fixed order:
+  //    part r goes to accumulator r % 4, combined as (a0 + a1) + (a2 + a3); sixteen independent
+  //    L2 loads in flight per step, the last step guarded (the sum is latency-bound)
   for (int e = tid; e < m * s; e += blockDim.x) {
     const int j = e % m, c = e / m;
-    double acc = 0.0;
-    for (int r = 0; r < a.nparts; ++r) acc += a.W[(size_t)r * a.w_stride + j + (int64_t)c * a.ldw];
-    sW[j + c * m] = acc;
+    const double* w = a.W + j + (int64_t)c * a.ldw;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = 0; r < a.nparts; r += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = r + u < a.nparts ? __ldcg(w + (size_t)(r + u) * a.w_stride) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u & 3] += v[u];
+    }
+    sW[j + c * m] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
   __syncthreads();
-  // 2. S = G - P^T P
+  FB_TR(1);
+  // 2. S = G - P^T P (four independent partial dot products per entry)
   for (int e = tid; e < s * s; e += blockDim.x) {
     const int x = e % s, y = e / s;
-    double ptp = 0.0;
-    for (int i = 0; i < k; ++i) ptp += sW[i + x * m] * sW[i + y * m];
-    sS[x + y * kSMax] = sW[k + x + y * m] - ptp;
+    const double* px = sW + x * m;
+    const double* py = sW + y * m;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    int i = 0;
+    for (; i + 4 <= k; i += 4) {
+      p0 += px[i] * py[i];
+      p1 += px[i + 1] * py[i + 1];
+      p2 += px[i + 2] * py[i + 2];
+      p3 += px[i + 3] * py[i + 3];
+    }
+    for (; i < k; ++i) p0 += px[i] * py[i];
+    sS[x + y * kSMax] = sW[k + x + y * m] - ((p0 + p1) + (p2 + p3));
   }
   for (int e = tid; e < kSMax * kSMax; e += blockDim.x) { sN[e] = 0.0; sNi[e] = 0.0; }
   __syncthreads();
+  FB_TR(2);
   // 3. in-order right-looking Cholesky with deflation (warp 0)
   if (tid < 32) {
     const int lane = tid;
@@ -203,9 +239,12 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs a) {
       const double gjj = sW[k + j + j * m];
       const double thr = fmax(thr_abs, a.eta * gjj);
       if (!(d > thr)) continue;  // deflated column (also catches NaN)
-      const double njj = sqrt(d);
-      if (lane == 0) { sN[r + j * kSMax] = njj; sPiv[r] = j; }
-      if (lane > j && lane < s) sN[r + lane * kSMax] = sS[j + lane * kSMax] / njj;
+      // pivot sqrt(d) and its inverse from one reciprocal square root (no fp64 division on
+      // the latency-bound critical path)
+      const double inv = rsqrt(d);
+      const double njj = d * inv;
+      if (lane == 0) { sN[r + j * kSMax] = njj; sPiv[r] = j; sInv[r] = inv; }
+      if (lane > j && lane < s) sN[r + lane * kSMax] = sS[j + lane * kSMax] * inv;
       __syncwarp();
       for (int e = lane; e < s * s; e += 32) {
         const int x = e % s, y = e / s;
@@ -220,15 +259,16 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs a) {
     const int t = r;
     if (lane < t) {
       const int c = lane;
-      sNi[c + c * kSMax] = 1.0 / sN[c + sPiv[c] * kSMax];
+      sNi[c + c * kSMax] = sInv[c];
       for (int i = c - 1; i >= 0; --i) {
         double acc = 0.0;
         for (int q = i + 1; q <= c; ++q) acc += sN[i + sPiv[q] * kSMax] * sNi[q + c * kSMax];
-        sNi[i + c * kSMax] = -acc / sN[i + sPiv[i] * kSMax];
+        sNi[i + c * kSMax] = -acc * sInv[i];
       }
     }
   }
   __syncthreads();
+  FB_TR(3);
   const int t = sT;
   // 5. outputs of this pass: P, N, M, t, pivots
   for (int e = tid; e < k * a.s; e += blockDim.x) {
@@ -259,6 +299,7 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs a) {
     if (a.deflated) *a.deflated = s - t;
   }
   if (tid < kSMax && a.piv_out) a.piv_out[tid] = tid < t ? sPiv[tid] : -1;
+  FB_TR(4);
   // 6. recombination (second pass): P = P1 + P2 N1,  N = N2 N1
   if (a.P1) {
     const int t1 = s;  // this pass normalised the t1 columns of U1
@@ -278,6 +319,8 @@ __global__ void __launch_bounds__(256) k_factor(FactorArgs a) {
     if (tid == 0) *a.tf = t;
   }
 }
+
+__global__ void __launch_bounds__(256) k_factor(FactorArgs a) { factor_body(a); }
 
 // ----------------------------------------------------------------------------
 // a4: fused update  U = [Q X] M   (M is m x s, columns >= t zero)

@@ -18,6 +18,7 @@
 #include "tsqr_wy.cuh"
 #include "stream_kernels.cuh"
 #include "stream2_kernels.cuh"
+#include "small_kernels.cuh"
 #include "support_kernels.cuh"
 #include "exchange.cuh"
 
@@ -70,6 +71,18 @@ struct HostPipe {
   double* Uh = nullptr; int64_t lduh = 0;
 };
 
+// A call's arguments: repeated calls with the same key (device buffers, PQR_NO_APPEND, one rank)
+// replay a CUDA graph captured from the second such call (no per-kernel host launch cost).
+struct GraphKey {
+  const void* X = nullptr; int64_t ldx = 0; int s = 0; unsigned flags = 0;
+  const void* U = nullptr; int64_t ldu = 0; const void* P = nullptr; int ldp = 0;
+  const void* N = nullptr; int ldn = 0; int k = -1;
+  bool operator==(const GraphKey& o) const {
+    return X == o.X && ldx == o.ldx && s == o.s && flags == o.flags && U == o.U && ldu == o.ldu && P == o.P &&
+           ldp == o.ldp && N == o.N && ldn == o.ldn && k == o.k;
+  }
+};
+
 struct Ctx {
   pqr_config cfg{};
   cudaStream_t stream = nullptr;
@@ -99,6 +112,13 @@ struct Ctx {
   int device = 0;                  // the handle's CUDA device (made current at every entry point)
   pqr_stats st{};
   TsqrState* ts = nullptr;
+  // CUDA-graph replay of repeated calls (GraphKey)
+  GraphKey gcand{}, gkey{};
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;  // capture/replay stream when the handle's stream is the legacy
+                                   // default stream (which cannot be captured)
+  cudaEvent_t gev = nullptr;
+  int64_t g_launches = 0;  // kernels per replay
   // profiling (pqr_profile_enable)
   bool prof = false;
   pqr_profile prof_tot{};
@@ -600,6 +620,50 @@ int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts) {
   return PQR_OK;
 }
 
+// One-launch CholQR2 for small n (k_cholqr2_small).  PQR_EPLAN when the call does not qualify:
+// n above PQR_SMALL_MAX (default 32768) or its rows do not fit the CTAs' shared memory.
+int run_small(Ctx* h, const double* X, int64_t ldx, int s, bool single, double tol2, double eta, double* Ud,
+              int64_t ldud, double* Uappend) {
+  static const int64_t nmax = getenv("PQR_SMALL_MAX") ? atoll(getenv("PQR_SMALL_MAX")) : 32768;
+  const int64_t n = h->cfg.n_local;
+  const int k = h->k;
+  if (n > nmax) return PQR_EPLAN;
+  // rows per CTA: at least 256 (fewer partials to sum), at most what the shared memory holds
+  int R = (int)std::max<int64_t>(256, (n + h->sms - 1) / h->sms);
+  const size_t budget = 232448 - 28 * 1024;  // minus factor_body's static shared memory
+  while (R > 16 && small_smem(R, k, s) > budget) R -= 16;
+  const int G = (int)((n + R - 1) / R);
+  if (small_smem(R, k, s) > budget || G > h->sms || (int64_t)G * R < n) return PQR_EPLAN;
+  const size_t smem = small_smem(R, k, s);
+  if (ensure_smem(k_cholqr2_small, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return PQR_EPLAN;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cholqr2_small, kSmallThreads, smem) != cudaSuccess ||
+      per_sm * h->sms < G) {
+    cudaGetLastError();
+    return PQR_EPLAN;
+  }
+  const int m = k + s;
+  SmallArgs a{};
+  a.Q = h->basis; a.ldq = h->ld; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.R = R;
+  a.single = single ? 1 : 0; a.tol2 = tol2; a.eta = eta;
+  a.U = Ud; a.ldu = ldud; a.U2 = Uappend; a.ldu2 = h->ld;
+  a.part1 = h->partials; a.part2 = h->partials + (size_t)h->sms * m * s;
+  a.bar = h->ticket + 1;
+  a.Pf = h->Pf; a.ldp = std::max(1, k); a.Nf = h->Nf; a.ints = h->ints;
+  CUDA_TRY(cudaMemsetAsync(h->ticket + 1, 0, sizeof(unsigned int), h->stream));
+  {
+    PROF(h, PQR_K_UPDATE_GRAM);
+    void* args[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cholqr2_small, G, kSmallThreads, args, smem, h->stream));
+  }
+  ++h->st.kernel_launches;
+  CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
+  return PQR_OK;
+}
+
 // ---------------------------------------------------------------------------
 // CholQR2 (BCGS-PIP+) solve, Alg. 8 with the recombination of DESIGN.md R1.
 // ---------------------------------------------------------------------------
@@ -615,6 +679,11 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
   const double eta = h->cfg.gram_eta > 0 ? h->cfg.gram_eta : 1e-13;
   const bool single = (flags & PQR_SINGLE_PASS) != 0;
 
+  // small n, one rank: the whole call as one cooperative kernel (small_kernels.cuh)
+  if (h->hp.nch == 0 && !h->xc) {
+    const int rc = run_small(h, X, ldx, s, single, tol2, eta, Ud, ldud, Uappend);
+    if (rc != PQR_EPLAN) return rc;
+  }
   // pass 1: W1 = [Q X]^T X -> P1, N1, M1, t1 -> U1 = [Q X] M1
   const double* Wsum = nullptr;
   int nparts = 1;
@@ -865,6 +934,26 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   const bool append = !(flags & PQR_NO_APPEND);
   if (!append && !U) return PQR_EARG;
 
+  static const bool no_graph = getenv("PQR_NO_GRAPH") != nullptr;
+  GraphKey key;
+  key.X = X; key.ldx = ldx; key.s = s; key.flags = flags; key.U = U; key.ldu = ldu; key.P = P; key.ldp = ldp;
+  key.N = N; key.ldn = ldn; key.k = k;
+  if (h->gexec && !h->prof && key == h->gkey) {
+    if (h->gstream) {  // legacy default stream: replay on the handle's own stream behind it
+      CUDA_TRY(cudaEventRecord(h->gev, h->stream));
+      CUDA_TRY(cudaStreamWaitEvent(h->gstream, h->gev, 0));
+    }
+    CUDA_TRY(cudaGraphLaunch(h->gexec, h->gstream ? h->gstream : h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->gstream ? h->gstream : h->stream));
+    const int tg = h->h_ints[2];
+    h->st.kernel_launches += h->g_launches;
+    if ((flags & PQR_NO_DEFLATION) && h->h_ints[3] > 0) return PQR_EBREAKDOWN;
+    *t = tg;
+    h->st.calls += 1;
+    h->st.last_t = tg;
+    return PQR_OK;
+  }
+
   // stage host inputs (host X and U on one rank: pipelined in row chunks, HostPipe)
   const double* Xd = X;
   int64_t ldxd = ldx;
@@ -904,30 +993,84 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   }
   const double tau = h->cfg.defl_tol > 0 ? h->cfg.defl_tol : 1e-12;
   int tt = 0;
-  int rc;
-  if (h->cfg.variant == PQR_CHOLQR2) {
-    double* Uapp = (append && Ud != h->basis + (int64_t)k * h->ld) ? h->basis + (int64_t)k * h->ld : nullptr;
-    rc = cholqr2_solve(h, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
-  } else {
-    rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
+  // graph capture: the second consecutive call with the same key, device buffers only, one rank
+  const bool graphable = !no_graph && !append && !x_host && !u_host && Ud == U && !h->xc && !h->prof &&
+                         h->hp.nch == 0 && !(P && k > 0 && is_host_ptr(P)) && !(N && is_host_ptr(N));
+  bool capturing = false;
+  if (graphable && key == h->gcand) {
+    if (h->gexec) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+    if (!h->stream && !h->gstream) {
+      if (cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->gev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        if (h->gstream) cudaStreamDestroy(h->gstream);
+        h->gstream = nullptr;
+      }
+    }
+    if (!h->stream && h->gstream) {
+      // capture on the handle's own stream (the legacy stream cannot be captured)
+      CUDA_TRY(cudaEventRecord(h->gev, h->stream));
+      CUDA_TRY(cudaStreamWaitEvent(h->gstream, h->gev, 0));
+      h->stream = h->gstream;
+    }
+    capturing = h->stream && cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (!capturing) cudaGetLastError();
+  }
+  h->gcand = graphable ? key : GraphKey{};
+  const int64_t launches0 = h->st.kernel_launches;
+  auto enqueue = [&]() -> int {
+    int rc;
+    if (h->cfg.variant == PQR_CHOLQR2) {
+      double* Uapp = (append && Ud != h->basis + (int64_t)k * h->ld) ? h->basis + (int64_t)k * h->ld : nullptr;
+      rc = cholqr2_solve(h, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
+    } else {
+      rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
+    }
+    if (rc != PQR_OK) return rc;
+    // outputs (enqueued before the one synchronisation of the call)
+    TRY(hp_finish(h));
+    if (U && Ud != U && h->hp.nch == 0) {
+      CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, ldud * sizeof(double), n * sizeof(double), s,
+                                 cudaMemcpyDefault, h->stream));
+    }
+    if (P && k > 0)
+      CUDA_TRY(cudaMemcpy2DAsync(P, (size_t)ldp * sizeof(double), h->Pf, (size_t)std::max(1, k) * sizeof(double),
+                                 (size_t)k * sizeof(double), s, cudaMemcpyDefault, h->stream));
+    if (N)
+      CUDA_TRY(cudaMemcpy2DAsync(N, (size_t)ldn * sizeof(double), h->Nf, (size_t)kSMax * sizeof(double),
+                                 (size_t)s * sizeof(double), s, cudaMemcpyDefault, h->stream));
+    return PQR_OK;
+  };
+  int rc = enqueue();
+  if (capturing) {
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
+    if (rc == PQR_OK && ec == cudaSuccess && graph &&
+        cudaGraphInstantiate(&h->gexec, graph, 0) == cudaSuccess) {
+      h->gkey = key;
+      h->g_launches = h->st.kernel_launches - launches0;
+      rc = cudaGraphLaunch(h->gexec, h->stream) == cudaSuccess ? PQR_OK : PQR_ECUDA;
+    } else {
+      // capture failed: run the call uncaptured
+      cudaGetLastError();
+      h->gexec = nullptr;
+      h->gcand = GraphKey{};
+      if (rc == PQR_OK) rc = enqueue();
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (h->gstream && h->stream == h->gstream) {
+      h->stream = (cudaStream_t)h->cfg.stream;  // back to the legacy stream after this call
+      CUDA_TRY(cudaStreamSynchronize(h->gstream));
+    }
   }
   if (rc != PQR_OK) {
     if (h->hp.nch > 0) cudaStreamSynchronize(h->cstream);
     h->hp.nch = 0;
     return rc;
   }
-  // outputs (enqueued before the one synchronisation of the call)
-  TRY(hp_finish(h));
-  if (U && Ud != U && h->hp.nch == 0) {
-    CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, ldud * sizeof(double), n * sizeof(double), s,
-                               cudaMemcpyDefault, h->stream));
-  }
-  if (P && k > 0)
-    CUDA_TRY(cudaMemcpy2DAsync(P, (size_t)ldp * sizeof(double), h->Pf, (size_t)std::max(1, k) * sizeof(double),
-                               (size_t)k * sizeof(double), s, cudaMemcpyDefault, h->stream));
-  if (N)
-    CUDA_TRY(cudaMemcpy2DAsync(N, (size_t)ldn * sizeof(double), h->Nf, (size_t)kSMax * sizeof(double),
-                               (size_t)s * sizeof(double), s, cudaMemcpyDefault, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->hp.nch = 0;
   prof_collect(h);
@@ -1007,6 +1150,9 @@ int pqr_destroy(pqr_handle hh) {
     cudaStreamDestroy(h->cstream);
   }
   delete h->xc;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
+  if (h->gev) cudaEventDestroy(h->gev);
   for (auto& p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   delete h;
@@ -1040,6 +1186,14 @@ int pqr_get_profile(pqr_handle hh, pqr_profile* out) {
   *out = h->prof_tot;
   return PQR_OK;
 }
+
+#ifdef PQR_SMALL_TRACE
+int pqr_small_trace(unsigned long long* out16) {
+  if (cudaMemcpyFromSymbol(out16, g_small_trace, 9 * sizeof(unsigned long long)) != cudaSuccess) return PQR_ECUDA;
+  return cudaMemcpyFromSymbol(out16 + 9, g_factor_trace, 5 * sizeof(unsigned long long)) == cudaSuccess ? PQR_OK
+                                                                                                       : PQR_ECUDA;
+}
+#endif
 
 int pqr_vgroup_create(int nranks, void** out) {
   if (!out || nranks < 1 || nranks > 1024) return PQR_EARG;

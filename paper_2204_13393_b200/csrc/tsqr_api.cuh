@@ -32,6 +32,9 @@ struct TsqrState {
   std::vector<int4> panels;  // committed panels (start, width, T offset, merged)
   int4* d_pan = nullptr;     // device copy (+ one uncommitted slot)
   int4* d_panm = nullptr;    // down-sweep list of a merging call
+  std::vector<int4> pan_mirror, panm_mirror;  // host copies of d_pan / d_panm (copy only on change:
+                                              // a repeated call enqueues no host-to-device copy, so
+                                              // it can be captured in a CUDA graph)
   int merge = 0, mtoff = 0;  // the last call merged its panel into the previous one
   double* in_top = nullptr;  // cap x wmax: GPU root stage-1 output (ld cap)
   double* xraw = nullptr;    // nranks * cap * wmax allgather receive (compact (C+s) x s blocks)
@@ -312,12 +315,22 @@ int run_top(Ctx* h, int s, bool build, double* P, int ldp, double* N, int ldn, i
 }
 
 // register the new panel (C, s) in the device list at slot np (uncommitted)
+bool int4_eq(const int4& a, const int4& b) { return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w; }
+
+// d_pan[i] = v (host-to-device copy only when the device copy differs)
+int set_pan(Ctx* h, int i, const int4& v) {
+  TsqrState* ts = h->ts;
+  if (ts->pan_mirror.size() <= (size_t)i) ts->pan_mirror.resize(i + 1, make_int4(-1, -1, -1, -1));
+  if (int4_eq(ts->pan_mirror[i], v)) return PQR_OK;
+  ts->pan_mirror[i] = v;
+  CUDA_TRY(cudaMemcpyAsync(ts->d_pan + i, &ts->pan_mirror[i], sizeof(int4), cudaMemcpyHostToDevice, h->stream));
+  return PQR_OK;
+}
+
 int tsqr_stage_panel(Ctx* h, int s) {
   TsqrState* ts = h->ts;
   const int np = (int)ts->panels.size();
-  const int4 pn = make_int4(ts->C, s, 16 * ts->C, 0);
-  CUDA_TRY(cudaMemcpyAsync(ts->d_pan + np, &pn, sizeof(int4), cudaMemcpyHostToDevice, h->stream));
-  return PQR_OK;
+  return set_pan(h, np, make_int4(ts->C, s, 16 * ts->C, 0));
 }
 
 // commit: R_top[:, k..k+t) = U~[0:C+s, 0:t);  panel (C, s) committed — or, when the call
@@ -333,7 +346,7 @@ int tsqr_commit(Ctx* h, int s, int t, int merge = 0, int mtoff = 0) {
     int4& pv = ts->panels.back();
     pv = make_int4(pv.x, pv.y + s, mtoff, 1);
     const int np = (int)ts->panels.size();
-    CUDA_TRY(cudaMemcpyAsync(ts->d_pan + np - 1, &pv, sizeof(int4), cudaMemcpyHostToDevice, h->stream));
+    TRY(set_pan(h, np - 1, pv));
   } else {
     ts->panels.push_back(make_int4(ts->C, s, 16 * ts->C, 0));
   }
@@ -530,7 +543,13 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
   if (ts->merge) {
     std::vector<int4> lst(ts->panels);
     lst.back() = make_int4(lst.back().x, 8, ts->mtoff, 1);
-    CUDA_TRY(cudaMemcpyAsync(ts->d_panm, lst.data(), sizeof(int4) * np, cudaMemcpyHostToDevice, h->stream));
+    bool same = ts->panm_mirror.size() == lst.size();
+    for (size_t i = 0; same && i < lst.size(); ++i) same = int4_eq(ts->panm_mirror[i], lst[i]);
+    if (!same) {
+      ts->panm_mirror = lst;
+      CUDA_TRY(cudaMemcpyAsync(ts->d_panm, ts->panm_mirror.data(), sizeof(int4) * np, cudaMemcpyHostToDevice,
+                               h->stream));
+    }
     TRY(tsqr_down_sweep(h, np, ts->C + s, ts->Ut, s, s, Ud, ldud, ts->d_panm, true));
   } else {
     TRY(tsqr_stage_panel(h, s));
