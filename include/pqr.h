@@ -59,6 +59,19 @@ typedef struct pqr_ctx* pqr_handle;
 
 typedef enum { PQR_CHOLQR2 = 0, PQR_TSQR = 1 } pqr_variant;
 
+/* PQR_TSQR: the reduction subalgorithm above the GPU's local Householder tree (§4,
+ * "local" and "reduction" subalgorithms; fig:architecture, L1186-1204, maps a reduction by
+ * BCGS-PIP+ onto the message-passing level):
+ *   PQR_REDUCTION_HH   — Householder: an arity-bounded tree over the GPU roots' (C+s) x s blocks,
+ *                        replicated on every GPU, then the top Householder solve with deflation
+ *                        (stable at any condition number);
+ *   PQR_REDUCTION_PIP2 — BCGS-PIP+ (Alg. 8) on the stacked GPU-root coordinates: two Gram
+ *                        exchanges of (k+s) x s per call; each GPU keeps its own top coordinates
+ *                        of the basis.  Stable only while eps*kappa^2 <= 1/2;
+ *                        beyond, orthogonality is lost (the call does not fail). */
+#define PQR_REDUCTION_HH   0
+#define PQR_REDUCTION_PIP2 1
+
 /* flags of pqr_project_normalize */
 #define PQR_NO_APPEND     1u  /* do not append U to the basis (k unchanged)          */
 #define PQR_NO_DEFLATION  2u  /* return PQR_EBREAKDOWN instead of deflating (t < s)  */
@@ -80,6 +93,7 @@ typedef struct {
                            nranks handles of this group live in ONE process on one device
                            and exchange through device copies instead of NCCL (see
                            pqr_vgroup_create); nccl_id is then ignored.                     */
+  int reduction;        /* PQR_TSQR: PQR_REDUCTION_HH (default) or PQR_REDUCTION_PIP2          */
 } pqr_config;
 
 /* Create a handle owning the basis (capacity k_max + s_max columns), its workspaces

@@ -593,12 +593,18 @@ int run_update_gram(int64_t n, int k, int s, const double* Q, int64_t ldq, const
 // Gram of this rank, then (nranks > 1) allgather so every rank sums all ranks'
 // partial Grams in rank order inside k_factor (bitwise identical replicas).
 int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts);
-int gram_and_exchange(Ctx* h, int k, int s, const double* Q, const double* X, int64_t ldx, const double** Wsum,
+// The basis a CholQR2 solve works on: the handle's explicit basis (CholQR2 variant), or a TSQR
+// handle's top coordinates R_g with the GPU root's block (TSQR with reduction = PIP+).
+struct BasisView {
+  const double* Q; int64_t ldq; int64_t n;
+};
+
+int gram_and_exchange(Ctx* h, const BasisView& bv, int k, int s, const double* X, int64_t ldx, const double** Wsum,
                       int* nparts) {
   const int m = k + s;
   {
     PROF(h, PQR_K_GRAM);
-    TRY(run_gram(h->cfg.n_local, k, s, Q, h->ld, X, ldx, h->Wloc, m, h->partials, h->ticket, h->sms, h->stream,
+    TRY(run_gram(bv.n, k, s, bv.Q, bv.ldq, X, ldx, h->Wloc, m, h->partials, h->ticket, h->sms, h->stream,
                  &h->st.kernel_launches));
   }
   return exchange(h, m, s, Wsum, nparts);
@@ -622,10 +628,10 @@ int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts) {
 
 // One-launch CholQR2 for small n (k_cholqr2_small).  PQR_EPLAN when the call does not qualify:
 // n above PQR_SMALL_MAX (default 32768) or its rows do not fit the CTAs' shared memory.
-int run_small(Ctx* h, const double* X, int64_t ldx, int s, bool single, double tol2, double eta, double* Ud,
-              int64_t ldud, double* Uappend) {
+int run_small(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, bool single, double tol2, double eta,
+              double* Ud, int64_t ldud, double* Uappend) {
   static const int64_t nmax = getenv("PQR_SMALL_MAX") ? atoll(getenv("PQR_SMALL_MAX")) : 32768;
-  const int64_t n = h->cfg.n_local;
+  const int64_t n = bv.n;
   const int k = h->k;
   if (n > nmax) return PQR_EPLAN;
   // rows per CTA: at least 256 (fewer partials to sum), at most what the shared memory holds
@@ -647,7 +653,7 @@ int run_small(Ctx* h, const double* X, int64_t ldx, int s, bool single, double t
   }
   const int m = k + s;
   SmallArgs a{};
-  a.Q = h->basis; a.ldq = h->ld; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.R = R;
+  a.Q = bv.Q; a.ldq = bv.ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.R = R;
   a.single = single ? 1 : 0; a.tol2 = tol2; a.eta = eta;
   a.U = Ud; a.ldu = ldud; a.U2 = Uappend; a.ldu2 = h->ld;
   a.part1 = h->partials; a.part2 = h->partials + (size_t)h->sms * m * s;
@@ -667,11 +673,11 @@ int run_small(Ctx* h, const double* X, int64_t ldx, int s, bool single, double t
 // ---------------------------------------------------------------------------
 // CholQR2 (BCGS-PIP+) solve, Alg. 8 with the recombination of DESIGN.md R1.
 // ---------------------------------------------------------------------------
-int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, double* Ud, int64_t ldud,
-                  double* Uappend, int* t_host, double tau) {
+int cholqr2_solve(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, unsigned flags, double* Ud,
+                  int64_t ldud, double* Uappend, int* t_host, double tau) {
   const int k = h->k;
   const int m = k + s;
-  const int64_t n = h->cfg.n_local;
+  const int64_t n = bv.n;
   int* d_t1 = h->ints + 0;
   int* d_t2 = h->ints + 1;
   int* d_def = h->ints + 3;
@@ -681,7 +687,7 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
 
   // small n, one rank: the whole call as one cooperative kernel (small_kernels.cuh)
   if (h->hp.nch == 0 && !h->xc) {
-    const int rc = run_small(h, X, ldx, s, single, tol2, eta, Ud, ldud, Uappend);
+    const int rc = run_small(h, bv, X, ldx, s, single, tol2, eta, Ud, ldud, Uappend);
     if (rc != PQR_EPLAN) return rc;
   }
   // pass 1: W1 = [Q X]^T X -> P1, N1, M1, t1 -> U1 = [Q X] M1
@@ -693,13 +699,13 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
     for (int c = 0; c < h->hp.nch; ++c) {
       const int64_t r0 = h->hp.r[c];
       TRY(hp_wait_in(h, c));
-      TRY(run_gram(h->hp.r[c + 1] - r0, k, s, h->basis + r0, h->ld, X + r0, ldx, h->Wchunks + (size_t)c * m * s, m,
+      TRY(run_gram(h->hp.r[c + 1] - r0, k, s, bv.Q + r0, bv.ldq, X + r0, ldx, h->Wchunks + (size_t)c * m * s, m,
                    h->partials, h->ticket, h->sms, h->stream, &h->st.kernel_launches));
     }
     Wsum = h->Wchunks;
     nparts = h->hp.nch;
   } else {
-    TRY(gram_and_exchange(h, k, s, h->basis, X, ldx, &Wsum, &nparts));
+    TRY(gram_and_exchange(h, bv, k, s, X, ldx, &Wsum, &nparts));
   }
   FactorArgs f{};
   f.W = Wsum; f.w_stride = (int64_t)m * s; f.nparts = nparts; f.ldw = m; f.k = k; f.s = s; f.s_dev = nullptr;
@@ -716,7 +722,7 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
     int rc;
     {
       PROF(h, PQR_K_UPDATE_GRAM);
-      rc = run_update_gram(n, k, s, h->basis, h->ld, X, ldx, h->M1, m, d_t1, Ud, ldud, h->Wloc, m, h->partials,
+      rc = run_update_gram(n, k, s, bv.Q, bv.ldq, X, ldx, h->M1, m, d_t1, Ud, ldud, h->Wloc, m, h->partials,
                            h->ticket, h->sms, h->stream, &h->st.kernel_launches);
     }
     if (rc == PQR_OK) {
@@ -728,12 +734,12 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
   }
   if (!fused) {
     PROF(h, PQR_K_UPDATE);
-    TRY(run_update(n, k, h->basis, h->ld, s, X, ldx, h->M1, m, s, d_t1, Ud, ldud, single ? Uappend : nullptr,
+    TRY(run_update(n, k, bv.Q, bv.ldq, s, X, ldx, h->M1, m, s, d_t1, Ud, ldud, single ? Uappend : nullptr,
                    h->ld, h->sms, h->stream, &h->st.kernel_launches));
   }
   if (!single) {
     // pass 2 on [Q U1]: W2 -> P2, N2, M2 (+ recombination) -> U = [Q U1] M2 (in place)
-    if (!fused) TRY(gram_and_exchange(h, k, s, h->basis, Ud, ldud, &Wsum, &nparts));
+    if (!fused) TRY(gram_and_exchange(h, bv, k, s, Ud, ldud, &Wsum, &nparts));
     FactorArgs f2{};
     f2.W = Wsum; f2.w_stride = (int64_t)m * s; f2.nparts = nparts; f2.ldw = m; f2.k = k; f2.s = s; f2.s_dev = d_t1;
     f2.tol2 = 0.0; f2.eta = 0.0;
@@ -750,13 +756,13 @@ int cholqr2_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, d
       PROF(h, PQR_K_UPDATE);
       for (int c = 0; c < h->hp.nch; ++c) {
         const int64_t r0 = h->hp.r[c];
-        TRY(run_update(h->hp.r[c + 1] - r0, k, h->basis + r0, h->ld, s, Ud + r0, ldud, h->M2, m, s, d_t2, Ud + r0,
+        TRY(run_update(h->hp.r[c + 1] - r0, k, bv.Q + r0, bv.ldq, s, Ud + r0, ldud, h->M2, m, s, d_t2, Ud + r0,
                        ldud, Uappend ? Uappend + r0 : nullptr, h->ld, h->sms, h->stream, &h->st.kernel_launches));
         TRY(hp_d2h_chunk(h, c, Ud, ldud, s));
       }
     } else {
       PROF(h, PQR_K_UPDATE);
-      TRY(run_update(n, k, h->basis, h->ld, s, Ud, ldud, h->M2, m, s, d_t2, Ud, ldud, Uappend, h->ld, h->sms,
+      TRY(run_update(n, k, bv.Q, bv.ldq, s, Ud, ldud, h->M2, m, s, d_t2, Ud, ldud, Uappend, h->ld, h->sms,
                      h->stream, &h->st.kernel_launches));
     }
   } else {
@@ -805,6 +811,7 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
     return PQR_EARG;
   if (cfg->k_max + cfg->s_max > kMMax) return PQR_ECAPACITY;
   if (cfg->variant != PQR_CHOLQR2 && cfg->variant != PQR_TSQR) return PQR_EARG;
+  if (cfg->reduction != PQR_REDUCTION_HH && cfg->reduction != PQR_REDUCTION_PIP2) return PQR_EARG;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return PQR_EARG;
   if (cfg->nranks > 1 && !cfg->nccl_id && !cfg->vgroup) return PQR_EARG;
   if (k > 0 && (!Q || ldq < cfg->n_local)) return PQR_EARG;
@@ -1025,7 +1032,7 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
     int rc;
     if (h->cfg.variant == PQR_CHOLQR2) {
       double* Uapp = (append && Ud != h->basis + (int64_t)k * h->ld) ? h->basis + (int64_t)k * h->ld : nullptr;
-      rc = cholqr2_solve(h, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
+      rc = cholqr2_solve(h, BasisView{h->basis, h->ld, n}, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
     } else {
       rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
     }

@@ -44,6 +44,9 @@ struct TsqrState {
   double* coef = nullptr;    // cap x 16 scratch for basis_apply
 };
 
+// reduction = PIP+ above the GPU tree (pqr.h PQR_REDUCTION_PIP2): no cross-GPU Householder levels
+bool pip2(const Ctx* h) { return h->cfg.reduction == PQR_REDUCTION_PIP2; }
+
 // units of 16 rows per warp: even (the stage-1 tail gives every lane UW/2 whole rows)
 int uw_for(int64_t rows) {
   const int uw = (int)((rows + kWyRowsPerUW - 1) / kWyRowsPerUW);
@@ -209,7 +212,7 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
   {
     PROF(h, PQR_K_TSQR_LOCAL);
     // the GPU root's block goes compact ((C+s) x s, ld C+s) when it is all-gathered
-    const int64_t ldtop = h->xc ? C + s : ts->cap;
+    const int64_t ldtop = h->xc && !pip2(h) ? C + s : ts->cap;
     double* out0 = ts->nlev >= 1 ? ts->lv[1].in : ts->in_top;
     const int64_t ldo0 = ts->nlev >= 1 ? ts->lv[1].rows : ldtop;
     if (pipe && h->hp.nch > 0) {
@@ -224,14 +227,14 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
   }
   {
     PROF(h, PQR_K_TSQR_TREE);
-    const int64_t ldtop = h->xc ? C + s : ts->cap;
+    const int64_t ldtop = h->xc && !pip2(h) ? C + s : ts->cap;
     for (int l = 1; l <= ts->nlev; ++l) {
       const bool root = l == ts->nlev;
       TRY(run_wy_up(h, ts->lv[l], ts->lv[l].in, ts->lv[l].rows, root ? ts->in_top : ts->lv[l + 1].in,
                     root ? ldtop : ts->lv[l + 1].rows, np, C, s, merge, mtoff));
     }
   }
-  if (h->xc) {
+  if (h->xc && !pip2(h)) {
     const int P = h->cfg.nranks;
     const size_t cnt = (size_t)(C + s) * s;
     {
@@ -265,7 +268,7 @@ int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol
   int64_t root_ld = ts->cap;
   {
     PROF(h, PQR_K_TSQR_TREE);
-    if (h->xc) {
+    if (h->xc && !pip2(h)) {
       // the replicated cross-GPU levels, top down; this rank's root is child `rank` of the
       // first cross level
       const int nx = (int)ts->xlv.size();
@@ -312,6 +315,22 @@ int run_top(Ctx* h, int s, bool build, double* P, int ldp, double* N, int ldn, i
   ++h->st.kernel_launches;
   CUDA_TRY(cudaGetLastError());
   return PQR_OK;
+}
+
+// reduction = PIP+ (PQR_REDUCTION_PIP2): BCGS-PIP+ (Alg. 8) of the GPU root's block B_g (C+s rows)
+// against this GPU's top coordinates R_g of the basis (Q = blockdiag(L_g) [R_0; ...; R_{P-1}],
+// L_g the GPU's locally orthogonal basis): the CholQR2 orchestration on (C+s)-row matrices, with
+// its two (k+s) x s Gram exchanges; the coordinates of U land in Ut (ld cap) for the down sweep.
+int run_pip2_top(Ctx* h, int s, unsigned flags) {
+  TsqrState* ts = h->ts;
+  const double tau = h->cfg.defl_tol > 0 ? h->cfg.defl_tol : 1e-12;
+  const int nch = h->hp.nch;  // the host-buffer pipeline concerns the leaf level only
+  h->hp.nch = 0;
+  int tt = 0;
+  const int rc = cholqr2_solve(h, BasisView{ts->Rt, ts->cap, ts->C + s}, ts->Btop, ts->cap, s,
+                               flags & (PQR_SINGLE_PASS | PQR_NO_DEFLATION), ts->Ut, ts->cap, nullptr, &tt, tau);
+  h->hp.nch = nch;
+  return rc;
 }
 
 // register the new panel (C, s) in the device list at slot np (uncommitted)
@@ -431,7 +450,7 @@ int tsqr_alloc(Ctx* h) {
   CUDA_TRY(cudaMemsetAsync(ts->Rt, 0, sizeof(double) * cap * cap, h->stream));
   if ((rc = dalloc(&ts->coef, (size_t)cap * 16))) return rc;
   if ((rc = dalloc(&ts->d_pan, (size_t)cap + 1)) || (rc = dalloc(&ts->d_panm, (size_t)cap + 1))) return rc;
-  if (h->xc) {
+  if (h->xc && !pip2(h)) {
     // cross-GPU levels over the nranks GPU roots, arity-bounded like the on-GPU node levels
     // (a level with more children than the arity is split into nodes of arity children; the
     // last level is one node of its children, an odd row count kept as the odd last row)
@@ -497,7 +516,13 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
   for (int c0 = 0; c0 < k; c0 += chunk) {
     const int cs = std::min(chunk, k - c0);
     TRY(tsqr_up_sweep(h, Q + (int64_t)c0 * ldq, ldq, cs));
-    TRY(run_top(h, cs, true, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
+    if (pip2(h)) {
+      // the chunk's coordinates are the new columns of R_g (Q = L [R; 0]: no PQR to solve)
+      CUDA_TRY(cudaMemcpy2DAsync(ts->Ut, ts->cap * sizeof(double), ts->in_top, ts->cap * sizeof(double),
+                                 (size_t)(ts->C + cs) * sizeof(double), cs, cudaMemcpyDeviceToDevice, h->stream));
+    } else {
+      TRY(run_top(h, cs, true, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
+    }
     TRY(tsqr_stage_panel(h, cs));
     TRY(tsqr_commit(h, cs, cs));
     h->k += cs;
@@ -538,7 +563,11 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
     }
   }
   TRY(tsqr_up_sweep(h, X, ldx, s, ts->merge, ts->mtoff, true));
-  TRY(run_top(h, s, false, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
+  if (pip2(h)) {
+    TRY(run_pip2_top(h, s, flags));
+  } else {
+    TRY(run_top(h, s, false, h->Pf, std::max(1, h->k), h->Nf, kSMax, h->ints + 2, h->ints + 3));
+  }
   // U~ columns >= t are zero, so the down sweep writes zeros there.
   if (ts->merge) {
     std::vector<int4> lst(ts->panels);

@@ -73,3 +73,46 @@ def run(pqr, Q, X, nranks, variant, calls=None, k_max=None, s_max=None, apply_af
 
 def gather_u(out, ci=0):
     return np.vstack([o["calls"][ci]["U"] for o in out])
+
+
+def block_qr(pqr, A, s, nranks, variant, **kw):
+    """Alg. 2 (block column QR) of the global host matrix A (n x m) on
+    `nranks` virtual ranks: rank r holds its row shard and appends every block's U.  Returns
+    the gathered n x k basis (host) and the t of each block."""
+    import torch
+
+    n, m = A.shape
+    g = pqr.pqr_vgroup_create(nranks)
+    out = [None] * nranks
+    errs = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            off, nl = row_shard(n, nranks, r)
+            st = torch.cuda.Stream()
+            Ad = dev(A[off:off + nl])
+            Qd = empty(nl, m)
+            torch.cuda.synchronize()
+            h = pqr.PQR(nl, m, s, None, k=0, variant=variant, stream=st, rank=r, nranks=nranks, vgroup=g, **kw)
+            k, ts = 0, []
+            for b in range(0, m, s):
+                w = min(s, m - b)
+                t = h.solve(Ad[:, b:b + w], U=Qd[:, k:k + w], s=w)
+                k += t
+                ts.append(t)
+            st.synchronize()
+            out[r] = dict(Q=host(Qd)[:, :k], t=ts)
+            h.close()
+        except Exception as e:  # pragma: no cover
+            errs.append((r, e))
+
+    ths = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    pqr.pqr_vgroup_destroy(g)
+    if errs:
+        raise errs[0][1]
+    return np.vstack([o["Q"] for o in out]), out[0]["t"]
