@@ -499,14 +499,14 @@ int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches) {
 int run_s2(int mode, const S2Args& a0, int sms, cudaStream_t st, int64_t* launches) {
   const int MT = (a0.k + a0.sx + 7) / 8;
   const int NT = (mode == kS2Gram ? a0.sx : a0.sout) > 8 ? 2 : 1;
-  if (MT > 20 || (NT == 2 && MT > 10)) return PQR_EPLAN;  // beyond: register spills
+  if (MT > 20) return PQR_EPLAN;
   const bool vec = (a0.k == 0 || ((a0.ldq & 1) == 0 && aligned16(a0.Q))) &&
                    (a0.sx == 0 || ((a0.ldx & 1) == 0 && aligned16(a0.X))) &&
                    (mode == kS2Gram || ((a0.ldu & 1) == 0 && aligned16(a0.U))) &&
                    (!a0.U2 || ((a0.ldu2 & 1) == 0 && aligned16(a0.U2)));
   if (!vec) return PQR_EPLAN;
   S2Args a = a0;
-  a.nslot = s2_nslot(MT, kSmemBudget);
+  a.nslot = s2_nslot(MT, NT, mode, kSmemBudget);
   // refill copies interleaved with the G phase: faster up to 12 tiles (config S: 2.14 -> 1.95 ms),
   // slower at 17 (weak config: 7.7 -> 9.3 ms); PQR_S2_IL=0|1 forces
   static const int env_il = getenv("PQR_S2_IL") ? atoi(getenv("PQR_S2_IL")) : -1;

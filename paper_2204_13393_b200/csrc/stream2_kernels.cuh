@@ -69,9 +69,14 @@ template <int MT, int NT, int MODE>
 __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
   constexpr bool DO_U = (MODE & kS2Update) != 0, DO_G = (MODE & kS2Gram) != 0;
   constexpr int MP = MT * 8, SLOT = MP * kS2Rows;  // doubles per slot
+  // two output tiles (NT = 2): the M fragments live in shared memory (in registers they would
+  // push the kernel past 255 registers: spills); one LDS.64 per k-step and tile
+  constexpr bool MSMEM = NT == 2 && DO_U;
+  constexpr int MFS = MSMEM ? 2 * MT * NT * 32 : 0;
   extern __shared__ __align__(128) double sm[];
   const int k = a.k, m = k + a.sx, NSL = a.nslot;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)NSL * SLOT);
+  double* sMf = sm + (size_t)NSL * SLOT;  // [2MT][NT][32 lanes] (MSMEM)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sMf + MFS);
   volatile int* fills = reinterpret_cast<volatile int*>(full + NSL);  // fills issued per slot
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
@@ -145,14 +150,20 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
   for (int i = warp; i < nu && i < NSL; i += kS2Consumers) issue(i, i, 0);
   {
     // ---------------- consumer warps ----------------
-    double mreg[DO_U ? 2 * MT : 1][NT];
+    double mreg[(DO_U && !MSMEM) ? 2 * MT : 1][NT];
 #pragma unroll
     for (int kk = 0; kk < (DO_U ? 2 * MT : 1); ++kk)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int j = 4 * kk + q, c = 8 * nt + g;
-        mreg[kk][nt] = (DO_U && j < m && c < a.sout) ? a.M[j + (int64_t)c * a.ldm] : 0.0;
+        const double v = (DO_U && j < m && c < a.sout) ? a.M[j + (int64_t)c * a.ldm] : 0.0;
+        if constexpr (MSMEM) {
+          if (warp == 0) sMf[(kk * NT + nt) * 32 + lane] = v;
+        } else {
+          mreg[kk][nt] = v;
+        }
       }
+    if constexpr (MSMEM) __syncthreads();
     const int tv = a.t_dev ? *a.t_dev : a.sout;
     const int offU = q * kS2Rows + 2 * (g ^ s2_swz(q));  // column 4kk+q, pair g (+ kk*64)
     const int sg = s2_swz(g & 3);
@@ -214,8 +225,11 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
           const double2 b = lds2(slot + offU + kk * 64);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
-            dmma884(dx[nt][kk & 1][0], dx[nt][kk & 1][1], mreg[kk][nt], b.x);
-            dmma884(dy[nt][kk & 1][0], dy[nt][kk & 1][1], mreg[kk][nt], b.y);
+            double mv;
+            if constexpr (MSMEM) mv = sMf[(kk * NT + nt) * 32 + lane];
+            else mv = mreg[kk][nt];
+            dmma884(dx[nt][kk & 1][0], dx[nt][kk & 1][1], mv, b.x);
+            dmma884(dy[nt][kk & 1][0], dy[nt][kk & 1][1], mv, b.y);
           }
         }
         const int64_t row = (ub + i) * kS2Rows + 4 * q;
@@ -375,12 +389,16 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
 // host: shared-memory slots for MT tiles of 8 columns (>= 9: every warp holds one while
 // another is in flight), and the launch.  Defined in stream2_*.cu (one translation unit
 // per mode, compiled in parallel).
-inline int s2_nslot(int MT, size_t budget) {
-  const size_t slot = (size_t)MT * 8 * kS2Rows * sizeof(double) + sizeof(uint64_t) + sizeof(int);
-  return (int)std::min<size_t>(24, (budget - 1024) / slot);
+inline size_t s2_mfs(int MT, int NT, int mode) {
+  return (NT == 2 && (mode & kS2Update)) ? (size_t)2 * MT * NT * 32 * sizeof(double) : 0;
 }
-inline size_t s2_smem(int MT, int nslot) {
-  return (size_t)nslot * MT * 8 * kS2Rows * sizeof(double) + (size_t)nslot * (sizeof(uint64_t) + sizeof(int));
+inline int s2_nslot(int MT, int NT, int mode, size_t budget) {
+  const size_t slot = (size_t)MT * 8 * kS2Rows * sizeof(double) + sizeof(uint64_t) + sizeof(int);
+  return (int)std::min<size_t>(24, (budget - 1024 - s2_mfs(MT, NT, mode)) / slot);
+}
+inline size_t s2_smem(int MT, int NT, int mode, int nslot) {
+  return (size_t)nslot * MT * 8 * kS2Rows * sizeof(double) + s2_mfs(MT, NT, mode) +
+         (size_t)nslot * (sizeof(uint64_t) + sizeof(int));
 }
 
 }  // namespace pqr

@@ -7,7 +7,7 @@ namespace {
 template <int MT, int NT>
 cudaError_t go(const S2Args& a, int grid, cudaStream_t st) {
   auto f = k_stream2<MT, NT, kS2Update>;
-  const size_t smem = s2_smem(MT, a.nslot);
+  const size_t smem = s2_smem(MT, NT, kS2Update, a.nslot);
   const cudaError_t e = ensure_smem(f, smem);
   if (e != cudaSuccess) return e;
   f<<<grid, kS2Threads, smem, st>>>(a);
