@@ -37,6 +37,9 @@
 
 namespace pqr {
 
+#ifndef PQR_S2_UCH
+#define PQR_S2_UCH 2  // U-phase accumulator chains per row half (2 or 4)
+#endif
 #ifndef PQR_S2_TG
 #define PQR_S2_TG 2  // G-phase tile group (1: each tile's four k-steps back to back; measured best: 2)
 #endif
@@ -215,11 +218,12 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
       const double* slot = sm + (size_t)sl * SLOT;
       double u[NT][4];
       if constexpr (DO_U) {
-        double dx[NT][2][2], dy[NT][2][2];
+        constexpr int UC = PQR_S2_UCH;
+        double dx[NT][UC][2], dy[NT][UC][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) dx[nt][e][0] = dx[nt][e][1] = dy[nt][e][0] = dy[nt][e][1] = 0.0;
+          for (int e = 0; e < UC; ++e) dx[nt][e][0] = dx[nt][e][1] = dy[nt][e][0] = dy[nt][e][1] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 2 * MT; ++kk) {
           const double2 b = lds2(slot + offU + kk * 64);
@@ -228,8 +232,8 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
             double mv;
             if constexpr (MSMEM) mv = sMf[(kk * NT + nt) * 32 + lane];
             else mv = mreg[kk][nt];
-            dmma884(dx[nt][kk & 1][0], dx[nt][kk & 1][1], mv, b.x);
-            dmma884(dy[nt][kk & 1][0], dy[nt][kk & 1][1], mv, b.y);
+            dmma884(dx[nt][kk % UC][0], dx[nt][kk % UC][1], mv, b.x);
+            dmma884(dy[nt][kk % UC][0], dy[nt][kk % UC][1], mv, b.y);
           }
         }
         const int64_t row = (ub + i) * kS2Rows + 4 * q;
@@ -237,10 +241,18 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
         for (int nt = 0; nt < NT; ++nt) {
           const int c = 8 * nt + g;
           const bool valid = c < tv;
-          u[nt][0] = valid ? dx[nt][0][0] + dx[nt][1][0] : 0.0;  // row 4q
-          u[nt][1] = valid ? dy[nt][0][0] + dy[nt][1][0] : 0.0;  // row 4q + 1
-          u[nt][2] = valid ? dx[nt][0][1] + dx[nt][1][1] : 0.0;  // row 4q + 2
-          u[nt][3] = valid ? dy[nt][0][1] + dy[nt][1][1] : 0.0;  // row 4q + 3
+          double sx0 = dx[nt][0][0] + dx[nt][1][0], sx1 = dx[nt][0][1] + dx[nt][1][1];
+          double sy0 = dy[nt][0][0] + dy[nt][1][0], sy1 = dy[nt][0][1] + dy[nt][1][1];
+          if constexpr (UC == 4) {
+            sx0 += dx[nt][2][0] + dx[nt][3][0];
+            sx1 += dx[nt][2][1] + dx[nt][3][1];
+            sy0 += dy[nt][2][0] + dy[nt][3][0];
+            sy1 += dy[nt][2][1] + dy[nt][3][1];
+          }
+          u[nt][0] = valid ? sx0 : 0.0;  // row 4q
+          u[nt][1] = valid ? sy0 : 0.0;  // row 4q + 1
+          u[nt][2] = valid ? sx1 : 0.0;  // row 4q + 2
+          u[nt][3] = valid ? sy1 : 0.0;  // row 4q + 3
           if (c < a.sout) {
             double* up = a.U + (int64_t)c * a.ldu + row;
             if (row + 3 < a.n) {

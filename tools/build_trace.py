@@ -2,7 +2,6 @@
 build/vtrace/ (the in-tree product library is untouched).  Run with
 PQR_LIB=$PWD/build/vtrace/libpqr.so PQR_WY_TRACE=1 python bench.py --variant tsqr ..."""
 import os
-import subprocess
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,8 +9,4 @@ from paper_2204_13393_b200 import build as b  # noqa: E402
 
 out = os.path.join(b.ROOT, "build", "vtrace", "libpqr.so")
 os.makedirs(os.path.dirname(out), exist_ok=True)
-inc, libdir = b.nccl_dirs()
-subprocess.check_call([b.NVCC, *b.ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-                       "-I", inc, "-I", os.path.join(b.ROOT, "include"), "-DPQR_WY_TRACE", *b.sources(), "-o", out,
-                       "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}", "-lcudart"])
-print(out)
+print(b.build(force=True, trace=True, out=out))
