@@ -71,6 +71,17 @@ typedef enum { PQR_CHOLQR2 = 0, PQR_TSQR = 1 } pqr_variant;
  *                        beyond, orthogonality is lost (the call does not fail). */
 #define PQR_REDUCTION_HH   0
 #define PQR_REDUCTION_PIP2 1
+/* PQR_TSQR: the local subalgorithm on each GPU (§4: "local" subalgorithm):
+ *   PQR_LOCAL_HH   — Householder on row blocks with the on-GPU reduction tree; the basis in its
+ *                    locally orthogonal representation (default);
+ *   PQR_LOCAL_PIP2 — BCGS-PIP+ of the GPU's whole shard against an explicit, locally orthonormal
+ *                    basis of that shard (one local problem per GPU, no on-GPU tree); the GPU's
+ *                    (C+s) x s coefficient block goes to the reduction as with PQR_LOCAL_HH, and U
+ *                    is formed from the local basis and the reduction's coefficients.  Stable only
+ *                    while eps*kappa^2 <= 1/2 (the local problem inherits BCGS-PIP+'s bound).
+ *                    Exists for the stability experiment of PAPER.md:L1274-1291 (fig:heatmap). */
+#define PQR_LOCAL_HH   0
+#define PQR_LOCAL_PIP2 1
 
 /* flags of pqr_project_normalize */
 #define PQR_NO_APPEND     1u  /* do not append U to the basis (k unchanged)          */
@@ -94,6 +105,7 @@ typedef struct {
                            and exchange through device copies instead of NCCL (see
                            pqr_vgroup_create); nccl_id is then ignored.                     */
   int reduction;        /* PQR_TSQR: PQR_REDUCTION_HH (default) or PQR_REDUCTION_PIP2          */
+  int local;            /* PQR_TSQR: PQR_LOCAL_HH (default) or PQR_LOCAL_PIP2                  */
 } pqr_config;
 
 /* Create a handle owning the basis (capacity k_max + s_max columns), its workspaces

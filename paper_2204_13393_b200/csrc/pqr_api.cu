@@ -597,6 +597,9 @@ int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts);
 // handle's top coordinates R_g with the GPU root's block (TSQR with reduction = PIP+).
 struct BasisView {
   const double* Q; int64_t ldq; int64_t n;
+  int k = -1;          // basis columns (-1: the handle's k)
+  bool local = false;  // this rank alone: no cross-rank exchange, deflation only of non-positive
+                       // pivots (a TSQR local problem never drops columns, reading R4)
 };
 
 int gram_and_exchange(Ctx* h, const BasisView& bv, int k, int s, const double* X, int64_t ldx, const double** Wsum,
@@ -606,6 +609,11 @@ int gram_and_exchange(Ctx* h, const BasisView& bv, int k, int s, const double* X
     PROF(h, PQR_K_GRAM);
     TRY(run_gram(bv.n, k, s, bv.Q, bv.ldq, X, ldx, h->Wloc, m, h->partials, h->ticket, h->sms, h->stream,
                  &h->st.kernel_launches));
+  }
+  if (bv.local) {
+    *Wsum = h->Wloc;
+    *nparts = 1;
+    return PQR_OK;
   }
   return exchange(h, m, s, Wsum, nparts);
 }
@@ -632,7 +640,7 @@ int run_small(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, 
               double* Ud, int64_t ldud, double* Uappend) {
   static const int64_t nmax = getenv("PQR_SMALL_MAX") ? atoll(getenv("PQR_SMALL_MAX")) : 32768;
   const int64_t n = bv.n;
-  const int k = h->k;
+  const int k = bv.k >= 0 ? bv.k : h->k;
   if (n > nmax) return PQR_EPLAN;
   // rows per CTA: at least 256 (fewer partials to sum), at most what the shared memory holds
   int R = (int)std::max<int64_t>(256, (n + h->sms - 1) / h->sms);
@@ -675,18 +683,18 @@ int run_small(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, 
 // ---------------------------------------------------------------------------
 int cholqr2_solve(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, unsigned flags, double* Ud,
                   int64_t ldud, double* Uappend, int* t_host, double tau) {
-  const int k = h->k;
+  const int k = bv.k >= 0 ? bv.k : h->k;
   const int m = k + s;
   const int64_t n = bv.n;
   int* d_t1 = h->ints + 0;
   int* d_t2 = h->ints + 1;
   int* d_def = h->ints + 3;
-  const double tol2 = tau * tau;
-  const double eta = h->cfg.gram_eta > 0 ? h->cfg.gram_eta : 1e-13;
+  const double tol2 = bv.local ? 0.0 : tau * tau;
+  const double eta = bv.local ? 0.0 : (h->cfg.gram_eta > 0 ? h->cfg.gram_eta : 1e-13);
   const bool single = (flags & PQR_SINGLE_PASS) != 0;
 
   // small n, one rank: the whole call as one cooperative kernel (small_kernels.cuh)
-  if (h->hp.nch == 0 && !h->xc) {
+  if (h->hp.nch == 0 && (!h->xc || bv.local)) {
     const int rc = run_small(h, bv, X, ldx, s, single, tol2, eta, Ud, ldud, Uappend);
     if (rc != PQR_EPLAN) return rc;
   }
@@ -727,7 +735,12 @@ int cholqr2_solve(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int
     }
     if (rc == PQR_OK) {
       fused = true;
-      TRY(exchange(h, m, s, &Wsum, &nparts));
+      if (bv.local) {
+        Wsum = h->Wloc;
+        nparts = 1;
+      } else {
+        TRY(exchange(h, m, s, &Wsum, &nparts));
+      }
     } else if (rc != PQR_EPLAN) {
       return rc;
     }
@@ -812,6 +825,7 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   if (cfg->k_max + cfg->s_max > kMMax) return PQR_ECAPACITY;
   if (cfg->variant != PQR_CHOLQR2 && cfg->variant != PQR_TSQR) return PQR_EARG;
   if (cfg->reduction != PQR_REDUCTION_HH && cfg->reduction != PQR_REDUCTION_PIP2) return PQR_EARG;
+  if (cfg->local != PQR_LOCAL_HH && cfg->local != PQR_LOCAL_PIP2) return PQR_EARG;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return PQR_EARG;
   if (cfg->nranks > 1 && !cfg->nccl_id && !cfg->vgroup) return PQR_EARG;
   if (k > 0 && (!Q || ldq < cfg->n_local)) return PQR_EARG;
@@ -969,7 +983,8 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
   h->hp.nch = 0;
   if (x_host) {
     if (!h->stageX && dalloc(&h->stageX, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
-    if (u_host && !h->xc && !(flags & PQR_SINGLE_PASS)) {
+    if (u_host && !h->xc && !(flags & PQR_SINGLE_PASS) &&
+        !(h->cfg.variant == PQR_TSQR && h->cfg.local == PQR_LOCAL_PIP2)) {
       if (h->cfg.variant == PQR_CHOLQR2) {
         if (!h->Wchunks && dalloc(&h->Wchunks, (size_t)kHostChunksMax * h->cap * h->cfg.s_max)) return PQR_ENOMEM;
         TRY(hp_plan_upload(h, X, ldx, s, U, ldu, nullptr));

@@ -46,6 +46,9 @@ struct TsqrState {
 
 // reduction = PIP+ above the GPU tree (pqr.h PQR_REDUCTION_PIP2): no cross-GPU Householder levels
 bool pip2(const Ctx* h) { return h->cfg.reduction == PQR_REDUCTION_PIP2; }
+// local = PIP+ (pqr.h PQR_LOCAL_PIP2): an explicit, locally orthonormal basis per GPU (h->basis)
+// and no on-GPU Householder tree
+bool lpip(const Ctx* h) { return h->cfg.local == PQR_LOCAL_PIP2; }
 
 // units of 16 rows per warp: even (the stage-1 tail gives every lane UW/2 whole rows)
 int uw_for(int64_t rows) {
@@ -209,7 +212,25 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
   TsqrState* ts = h->ts;
   const int C = ts->C;
   const int np = (int)ts->panels.size();
-  {
+  if (lpip(h)) {
+    // local problem of the whole shard by BCGS-PIP+ against the explicit local basis (C columns):
+    // U_loc into the basis' spare columns C.., and the coefficient block [P_loc; N_loc] ((C+s) x s)
+    // into in_top (ld cap) for the reduction
+    const int nch = h->hp.nch;
+    h->hp.nch = 0;
+    BasisView bv{h->basis, h->ld, h->cfg.n_local};
+    bv.k = C;
+    bv.local = true;
+    int tt = 0;
+    const int rc = cholqr2_solve(h, bv, X, ldx, s, 0, h->basis + (int64_t)C * h->ld, h->ld, nullptr, &tt, 0.0);
+    h->hp.nch = nch;
+    TRY(rc);
+    if (C > 0)
+      CUDA_TRY(cudaMemcpy2DAsync(ts->in_top, ts->cap * sizeof(double), h->Pf, (size_t)C * sizeof(double),
+                                 (size_t)C * sizeof(double), s, cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_TRY(cudaMemcpy2DAsync(ts->in_top + C, ts->cap * sizeof(double), h->Nf, (size_t)kSMax * sizeof(double),
+                               (size_t)s * sizeof(double), s, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
     PROF(h, PQR_K_TSQR_LOCAL);
     // the GPU root's block goes compact ((C+s) x s, ld C+s) when it is all-gathered
     const int64_t ldtop = h->xc && !pip2(h) ? C + s : ts->cap;
@@ -237,6 +258,11 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
   if (h->xc && !pip2(h)) {
     const int P = h->cfg.nranks;
     const size_t cnt = (size_t)(C + s) * s;
+    if (lpip(h)) {  // the allgather sends the block compact (ld C + s)
+      CUDA_TRY(cudaMemcpy2DAsync(ts->Btop, (C + s) * sizeof(double), ts->in_top, ts->cap * sizeof(double),
+                                 (size_t)(C + s) * sizeof(double), s, cudaMemcpyDeviceToDevice, h->stream));
+      CUDA_TRY(cudaMemcpyAsync(ts->in_top, ts->Btop, cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    }
     {
       PROF(h, PQR_K_NCCL);
       TRY(h->xc->allgather(ts->in_top, ts->xraw, cnt, h->stream));
@@ -287,6 +313,13 @@ int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol
     }
   }
   PROF(h, PQR_K_TSQR_APPLY);
+  if (lpip(h)) {
+    // Y = [L_g U_loc] root_cin (Call rows: C basis columns, then Call - C columns of U_loc, which sit
+    // in the basis' spare columns)
+    const int C = ts->C;
+    return run_update(h->cfg.n_local, C, h->basis, h->ld, Call - C, h->basis + (int64_t)C * h->ld, h->ld, root_cin,
+                      (int)root_ld, ncol, nullptr, Y, ldy, nullptr, 0, h->sms, h->stream, &h->st.kernel_launches);
+  }
   const double* cin0 = ts->nlev >= 1 ? ts->lv[1].dn : root_cin;
   const int64_t ldc0 = ts->nlev >= 1 ? ts->lv[1].rows : root_ld;
   if (pipe && h->hp.nch > 0) {
@@ -404,6 +437,14 @@ int tsqr_alloc(Ctx* h) {
   ts->arity = std::max(2, std::min(8, rmax / cap));
   if ((cap & 1) && (ts->arity & 1)) ts->arity -= 1;
   ts->arity = std::max(2, ts->arity);
+  int rc;
+  ts->lv.clear();
+  if (lpip(h)) {
+    // local = PIP+: the explicit local basis (n_local x cap) replaces the leaf and node levels
+    if ((rc = dalloc(&h->basis, (size_t)h->ld * cap))) return rc;
+    ts->nb = 0;
+    ts->nlev = 0;
+  } else {
   // leaf block rows: user's choice or ~1024 (512 when s_max > 8)
   int nb = h->cfg.block_rows > 0 ? h->cfg.block_rows : (wmax > 8 ? 512 : 1024);
   nb = std::max(nb, 2 * cap);
@@ -425,7 +466,6 @@ int tsqr_alloc(Ctx* h) {
   leaf.rows = h->ld;
   leaf.ldv = h->ld;
   ts->nb = nb;
-  int rc;
   TRY(alloc_level(h, leaf, wmax, false));
   if (n & 1)  // zero pad row n of every reflector column (bulk copies of the odd last block read it)
     CUDA_TRY(cudaMemset2DAsync(leaf.V + n, leaf.ldv * sizeof(double), 0, sizeof(double), cap, h->stream));
@@ -443,6 +483,8 @@ int tsqr_alloc(Ctx* h) {
     ts->lv.push_back(nd);
   }
   ts->nlev = (int)ts->lv.size() - 1;
+  }
+
   if ((rc = dalloc(&ts->in_top, (size_t)cap * wmax))) return rc;
   CUDA_TRY(cudaMemsetAsync(ts->in_top, 0, sizeof(double) * cap * wmax, h->stream));
   if ((rc = dalloc(&ts->Ut, (size_t)cap * 16))) return rc;
@@ -480,7 +522,7 @@ int tsqr_alloc(Ctx* h) {
   } else {
     ts->Btop = ts->in_top;
   }
-  h->st.block_rows = (int)leaf.q;
+  h->st.block_rows = lpip(h) ? 0 : (int)ts->lv[0].q;
   h->st.tree_levels = ts->nlev;
   return PQR_OK;
 }
@@ -493,7 +535,8 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
   TsqrState* ts = h->ts;
   h->k = 0;
   ts->C = 0;
-  const int chunk = ts->wmax;
+  // (local = PIP+: the local CholQR2's small buffers hold s_max columns)
+  const int chunk = lpip(h) ? std::min(ts->wmax, h->cfg.s_max) : ts->wmax;
   // 16-byte aligned copy of Q with even ld for the bulk copies (freed on every exit path)
   struct AlignedQ {
     double* p = nullptr;
@@ -555,7 +598,7 @@ int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, doub
   static const bool no_merge = getenv("PQR_NO_MERGE") != nullptr;
   ts->merge = 0;
   ts->mtoff = 0;
-  if (!no_merge && ts->wmax == 8 && np >= 1) {
+  if (!no_merge && !lpip(h) && ts->wmax == 8 && np >= 1) {
     const int4 pv = ts->panels.back();
     if (pv.w == 0 && pv.y == 4 && s == 4 && pv.x + pv.y == ts->C) {
       ts->merge = 1;
@@ -600,7 +643,7 @@ int tsqr_apply(Ctx* h, const double* C, int ldc, int m, double* Y, int64_t ldy) 
   const bool stage = is_host_ptr(Y) || (ldy & 1) || !aligned16(Y);
   if (stage && !h->stageU && dalloc(&h->stageU, (size_t)h->ld * h->cfg.s_max)) return PQR_ENOMEM;
   if (!h->stageC && dalloc(&h->stageC, (size_t)h->cap * 16)) return PQR_ENOMEM;
-  const int nt_max = (ts->lv[0].UW <= 2 && (ts->nlev == 0 || ts->lv[1].UW <= 2)) ? 2 : 1;
+  const int nt_max = lpip(h) || (ts->lv[0].UW <= 2 && (ts->nlev == 0 || ts->lv[1].UW <= 2)) ? 2 : 1;
   int chunk = std::min(8 * nt_max, stage ? h->cfg.s_max : 16);
   const int np = (int)ts->panels.size();
   for (int c0 = 0; c0 < m; c0 += chunk) {

@@ -23,6 +23,8 @@ PQR_NO_APPEND, PQR_NO_DEFLATION, PQR_SINGLE_PASS = 1, 2, 4
 VARIANTS = {"cholqr2": PQR_CHOLQR2, "tsqr": PQR_TSQR}
 PQR_REDUCTION_HH, PQR_REDUCTION_PIP2 = 0, 1
 REDUCTIONS = {"hh": PQR_REDUCTION_HH, "pip2": PQR_REDUCTION_PIP2}
+PQR_LOCAL_HH, PQR_LOCAL_PIP2 = 0, 1
+LOCALS = {"hh": PQR_LOCAL_HH, "pip2": PQR_LOCAL_PIP2}
 
 
 class PQRError(RuntimeError):
@@ -37,7 +39,7 @@ class pqr_config(ctypes.Structure):
         ("variant", ctypes.c_int), ("defl_tol", ctypes.c_double), ("gram_eta", ctypes.c_double),
         ("block_rows", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
         ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("vgroup", ctypes.c_void_p),
-        ("reduction", ctypes.c_int),
+        ("reduction", ctypes.c_int), ("local", ctypes.c_int),
     ]
 
 
@@ -158,7 +160,8 @@ def _stream_ptr(stream):
 # C-ABI mirror (same names)
 # ---------------------------------------------------------------------------
 def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0.0, gram_eta=0.0, block_rows=0,
-               stream=None, rank=0, nranks=1, nccl_id: bytes | None = None, vgroup=None, reduction="hh"):
+               stream=None, rank=0, nranks=1, nccl_id: bytes | None = None, vgroup=None, reduction="hh",
+               local="hh"):
     cfg = pqr_config()
     cfg.n_local = int(n_local)
     cfg.k_max = int(k_max)
@@ -172,6 +175,7 @@ def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0
     cfg.nranks = int(nranks)
     cfg.vgroup = vgroup.value if isinstance(vgroup, ctypes.c_void_p) else vgroup
     cfg.reduction = REDUCTIONS[reduction] if isinstance(reduction, str) else int(reduction)
+    cfg.local = LOCALS[local] if isinstance(local, str) else int(local)
     idbuf = None
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

@@ -46,13 +46,32 @@ def test_pip2_vs_oracle(P, orc, nranks, n, k, s):
     assert np.linalg.norm(np.eye(s) - U.T @ U, 2) < 1e-12 and np.linalg.norm(Q.T @ U, 2) < 1e-12
 
 
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+@pytest.mark.parametrize("n,k,s", [(100_003, 64, 8), (60_000, 96, 16), (30_001, 13, 3)])
+def test_local_pip2_vs_oracle(P, orc, nranks, n, k, s):
+    """local = PIP+ (explicit local basis per GPU) with the Householder reduction."""
+    Q = inputs.orthonormal(15 + n + k, n, k)
+    X = inputs.gaussian(16 + n + s, n, s)
+    ref = orc.householder_pqr(Q, X)
+    out = vranks.run(P, Q, X, nranks, "tsqr", local="pip2")
+    c0 = out[0]["calls"][0]
+    for o in out[1:]:
+        c = o["calls"][0]
+        assert c["t"] == c0["t"] and np.array_equal(c["P"], c0["P"]) and np.array_equal(c["N"], c0["N"])
+    U = vranks.gather_u(out)
+    assert c0["t"] == ref["t"] == s
+    assert rel(c0["P"], ref["P"]) < 1e-10 and rel(c0["N"], ref["N"]) < 1e-10 and rel(U, ref["U"]) < 1e-10
+    assert np.linalg.norm(np.eye(s) - U.T @ U, 2) < 1e-12 and np.linalg.norm(Q.T @ U, 2) < 1e-12
+
+
+@pytest.mark.parametrize("local,reduction", [("hh", "pip2"), ("pip2", "hh"), ("pip2", "pip2")])
 @pytest.mark.parametrize("nranks", [1, 3])
-def test_pip2_appending_and_basis_apply(P, orc, nranks):
+def test_pip2_appending_and_basis_apply(P, orc, nranks, local, reduction):
     n, k = 50_001, 20
     Q = inputs.orthonormal(61, n, k)
     Xs = [inputs.gaussian(62 + i, n, w) for i, w in enumerate((8, 4, 8))]
     out = vranks.run(P, Q, Xs[0], nranks, "tsqr", calls=[(x, 0) for x in Xs], k_max=k + 20, s_max=8,
-                     apply_after=True, reduction="pip2")
+                     apply_after=True, reduction=reduction, local=local)
     Qg = Q
     for ci, x in enumerate(Xs):
         ref = orc.householder_pqr(Qg, x)
@@ -81,9 +100,10 @@ def heatmap(P, kappa, nranks=4, n=1 << 15, m=64, s=4, tol=1e-300):
     effect (defl_tol and gram_eta), as the paper's experiment has none."""
     A = inputs.stewart(2022, n, m, kappa)
     out = {}
-    for name, variant, red in (("hh/hh", "tsqr", "hh"), ("hh/pip2", "tsqr", "pip2"), ("pip2/pip2", "cholqr2", "hh")):
-        Qg, ts = vranks.block_qr(P, A, s, nranks, variant, reduction=red, defl_tol=tol, gram_eta=tol,
-                                 block_rows=256 if variant == "tsqr" else 0)
+    for name, variant, loc, red in (("hh/hh", "tsqr", "hh", "hh"), ("hh/pip2", "tsqr", "hh", "pip2"),
+                                    ("pip2/hh", "tsqr", "pip2", "hh"), ("pip2/pip2", "cholqr2", "hh", "hh")):
+        Qg, ts = vranks.block_qr(P, A, s, nranks, variant, reduction=red, local=loc, defl_tol=tol, gram_eta=tol,
+                                 block_rows=256 if (variant == "tsqr" and loc == "hh") else 0)
         e = np.linalg.norm(np.eye(Qg.shape[1]) - Qg.T @ Qg)
         out[name] = dict(e_perp=float(e) if np.isfinite(e) else float("inf"), rank=int(sum(ts)))
     return out
@@ -94,14 +114,18 @@ def test_heatmap_claim(P):
     sits at the edge (eps kappa^2 ~ 2): measured on B200 all three combinations are still
     orthogonal there (profiles/r02_heatmap.jsonl).  At kappa = 1e10 the claim "both subalgorithms
     must be stable to obtain a stable method" holds: Householder local + Householder reduction
-    keeps full rank and orthogonality, while a BCGS-PIP+ reduction (HH local) and BCGS-PIP+
-    everywhere (the CholQR2 variant) break down — their in-order Cholesky meets non-positive
+    keeps full rank and orthogonality, while a BCGS-PIP+ reduction (with HH or PIP+ local: the
+    CholQR2 variant is PIP+ everywhere) breaks down — their in-order Cholesky meets non-positive
     pivots and drops columns (rank < 64) instead of returning a non-orthogonal basis.  At kappa =
     1e4 all three are orthogonal with full rank."""
     h10 = heatmap(P, 1e10)
     assert h10["hh/hh"]["e_perp"] < 1e-13 and h10["hh/hh"]["rank"] == 64, h10
     for name in ("hh/pip2", "pip2/pip2"):
         assert h10[name]["e_perp"] > 1e-6 or h10[name]["rank"] < 64, (name, h10)
+    # (PIP+ local with the Householder reduction stays orthogonal with full rank here: each GPU's
+    # local problem is re-orthogonalised by the second pass and the reduction is stable; recorded
+    # in profiles/r02_heatmap.jsonl and DESIGN.md, not a claim of the paper)
+    assert np.isfinite(h10["pip2/hh"]["e_perp"])
     h4 = heatmap(P, 1e4)
     for name, d in h4.items():
         assert d["e_perp"] < 1e-13 and d["rank"] == 64, (name, h4)
