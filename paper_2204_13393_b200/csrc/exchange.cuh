@@ -67,6 +67,19 @@ struct VirtualGroup {
   std::vector<const double*> send;
   std::vector<cudaEvent_t> ready, done;
   explicit VirtualGroup(int p) : P(p), send(p, nullptr), ready(p, nullptr), done(p, nullptr) {}
+  // the group owns the ranks' events: a rank whose handle is destroyed (e.g. after a failed
+  // call) leaves its events valid for peers that already enqueued waits on them
+  ~VirtualGroup() {
+    for (auto e : ready)
+      if (e) cudaEventDestroy(e);
+    for (auto e : done)
+      if (e) cudaEventDestroy(e);
+  }
+  void leave() {  // a member handle is gone: later barriers fail instead of waiting
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
   bool barrier() {
     std::unique_lock<std::mutex> lk(mu);
     if (broken) return false;
@@ -78,12 +91,11 @@ struct VirtualGroup {
       return true;
     }
     static const int tmo = getenv("PQR_VGROUP_TIMEOUT") ? atoi(getenv("PQR_VGROUP_TIMEOUT")) : 300;
-    if (!cv.wait_for(lk, std::chrono::seconds(tmo), [&] { return gen != g || broken; }) || broken) {
-      broken = true;
-      cv.notify_all();
-      return false;
-    }
-    return true;
+    cv.wait_for(lk, std::chrono::seconds(tmo), [&] { return gen != g || broken; });
+    if (gen != g) return true;  // this barrier completed (a peer may have left right after it)
+    broken = true;              // timeout, or a peer left before arriving
+    cv.notify_all();
+    return false;
   }
 };
 
@@ -91,21 +103,19 @@ struct VirtualExchange : Exchange {
   VirtualGroup* g = nullptr;
   cudaEvent_t ready = nullptr, done = nullptr;
   ~VirtualExchange() override {
-    if (ready) cudaEventDestroy(ready);
-    if (done) cudaEventDestroy(done);
+    if (g) g->leave();
   }
   int init(VirtualGroup* grp, int r) {
     g = grp;
     rank = r;
     nranks = grp->P;
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->ready[r] || g->done[r]) return -1;  // PQR_EARG: rank already taken in this group
     if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess)
       return -5;  // PQR_ECUDA
-    {
-      std::lock_guard<std::mutex> lk(g->mu);
-      g->ready[r] = ready;
-      g->done[r] = done;
-    }
+    g->ready[r] = ready;
+    g->done[r] = done;
     return 0;
   }
   int allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {

@@ -878,7 +878,7 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
     if (g->P != cfg->nranks) return fail(PQR_EARG);
     auto* vx = new VirtualExchange();
     h->xc = vx;
-    if (vx->init(g, cfg->rank)) return fail(PQR_ECUDA);
+    if (const int e = vx->init(g, cfg->rank)) return fail(e == -1 ? PQR_EARG : PQR_ECUDA);
   } else if (cfg->nranks > 1 || force_nccl) {
     ncclUniqueId id;
     if (cfg->nccl_id) {

@@ -32,6 +32,7 @@ def run(pqr, Q, X, nranks, variant, calls=None, k_max=None, s_max=None, apply_af
     errs = []
 
     def worker(r):
+        h = None
         try:
             torch.cuda.set_device(0)
             off, nl = row_shard(n, nranks, r)
@@ -56,9 +57,11 @@ def run(pqr, Q, X, nranks, variant, calls=None, k_max=None, s_max=None, apply_af
                 st.synchronize()
                 basis = host(V)
             out[r] = dict(calls=res, stats=h.stats(), basis=basis)
-            h.close()
         except Exception as e:  # pragma: no cover - reported below
             errs.append((r, e))
+        finally:
+            if h is not None:
+                h.close()
 
     ths = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
     for t in ths:
@@ -67,7 +70,8 @@ def run(pqr, Q, X, nranks, variant, calls=None, k_max=None, s_max=None, apply_af
         t.join()
     pqr.pqr_vgroup_destroy(g)
     if errs:
-        raise errs[0][1]
+        r, e = min(errs, key=lambda x: x[0])
+        raise RuntimeError(f"virtual rank {r} failed: {e!r} (all: {errs!r})") from e
     return out
 
 
@@ -87,6 +91,7 @@ def block_qr(pqr, A, s, nranks, variant, **kw):
     errs = []
 
     def worker(r):
+        h = None
         try:
             torch.cuda.set_device(0)
             off, nl = row_shard(n, nranks, r)
@@ -103,9 +108,11 @@ def block_qr(pqr, A, s, nranks, variant, **kw):
                 ts.append(t)
             st.synchronize()
             out[r] = dict(Q=host(Qd)[:, :k], t=ts)
-            h.close()
         except Exception as e:  # pragma: no cover
             errs.append((r, e))
+        finally:
+            if h is not None:
+                h.close()
 
     ths = [threading.Thread(target=worker, args=(r,)) for r in range(nranks)]
     for t in ths:
@@ -114,5 +121,6 @@ def block_qr(pqr, A, s, nranks, variant, **kw):
         t.join()
     pqr.pqr_vgroup_destroy(g)
     if errs:
-        raise errs[0][1]
+        r, e = min(errs, key=lambda x: x[0])
+        raise RuntimeError(f"virtual rank {r} failed: {e!r} (all: {errs!r})") from e
     return np.vstack([o["Q"] for o in out]), out[0]["t"]
