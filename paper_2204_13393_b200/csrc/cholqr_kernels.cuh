@@ -191,65 +191,79 @@ __device__ __forceinline__ void factor_body(const FactorArgs& a) {
   const int m = k + s;
 
   // 1. sum the per-part Gram matrices (ranks, host-buffer chunks, or CTAs) in a fixed order:
-  //    part r goes to accumulator r % 4, combined as (a0 + a1) + (a2 + a3); sixteen independent
-  //    L2 loads in flight per step, the last step guarded (the sum is latency-bound)
+  //    part r goes to accumulator r % 4, combined as (a0 + a1) + (a2 + a3); 48 independent
+  //    L2 loads in flight per step, the last step guarded (the sum is latency-bound: one step
+  //    covers a small-n call's CTA partials)
   for (int e = tid; e < m * s; e += blockDim.x) {
     const int j = e % m, c = e / m;
     const double* w = a.W + j + (int64_t)c * a.ldw;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int r = 0; r < a.nparts; r += 16) {
-      double v[16];
+    for (int r = 0; r < a.nparts; r += 48) {
+      double v[48];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = r + u < a.nparts ? __ldcg(w + (size_t)(r + u) * a.w_stride) : 0.0;
+      for (int u = 0; u < 48; ++u) v[u] = r + u < a.nparts ? __ldcg(w + (size_t)(r + u) * a.w_stride) : 0.0;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) acc[u & 3] += v[u];
+      for (int u = 0; u < 48; ++u) acc[u & 3] += v[u];
     }
     sW[j + c * m] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
   __syncthreads();
   FB_TR(1);
-  // 2. S = G - P^T P (four independent partial dot products per entry)
-  for (int e = tid; e < s * s; e += blockDim.x) {
-    const int x = e % s, y = e / s;
-    const double* px = sW + x * m;
-    const double* py = sW + y * m;
-    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-    int i = 0;
-    for (; i + 4 <= k; i += 4) {
-      p0 += px[i] * py[i];
-      p1 += px[i + 1] * py[i + 1];
-      p2 += px[i + 2] * py[i + 2];
-      p3 += px[i + 3] * py[i + 3];
+  // 2. S = G - P^T P: TP threads per entry (a power of two, the entries spread over the CTA),
+  //    each a strided partial dot product over the k rows of P, then a fixed xor tree
+  {
+    const int ss = s * s;
+    int TP = 1;
+    while (TP < 32 && TP * 2 * ss <= (int)blockDim.x) TP *= 2;
+    for (int base = 0; base < ss * TP; base += blockDim.x) {
+      const int e = (base + tid) / TP, part = (base + tid) % TP;
+      double p0 = 0.0, p1 = 0.0;
+      if (e < ss) {
+        const int x = e % s, y = e / s;
+        const double* px = sW + x * m;
+        const double* py = sW + y * m;
+        int i = part;
+        for (; i + TP < k; i += 2 * TP) {
+          p0 = fma(px[i], py[i], p0);
+          p1 = fma(px[i + TP], py[i + TP], p1);
+        }
+        if (i < k) p0 = fma(px[i], py[i], p0);
+      }
+      double p = p0 + p1;
+      for (int mb = 1; mb < TP; mb <<= 1) p += __shfl_xor_sync(0xffffffffu, p, mb);
+      if (e < ss && part == 0) {
+        const int x = e % s, y = e / s;
+        sS[x + y * kSMax] = sW[k + x + y * m] - p;
+      }
     }
-    for (; i < k; ++i) p0 += px[i] * py[i];
-    sS[x + y * kSMax] = sW[k + x + y * m] - ((p0 + p1) + (p2 + p3));
   }
   for (int e = tid; e < kSMax * kSMax; e += blockDim.x) { sN[e] = 0.0; sNi[e] = 0.0; }
   __syncthreads();
   FB_TR(2);
-  // 3. in-order right-looking Cholesky with deflation (warp 0)
+  // 3. in-order right-looking Cholesky with deflation (warp 0).  Lane x owns row x of the
+  //    trailing S (it alone updates it; S is symmetric, so the pivot row's entry S(j, x) is read
+  //    as S(x, j) from the lane's own row): one warp synchronisation per column.
   if (tid < 32) {
     const int lane = tid;
     double trace = 0.0;
     for (int c = 0; c < s; ++c) trace += sW[k + c + c * m];
     const double thr_abs = a.tol2 * trace;
+    double* Srow = sS + lane;  // row `lane`: Srow[y * kSMax] = S(lane, y)
     int r = 0;
     for (int j = 0; j < s; ++j) {
       const double d = sS[j + j * kSMax];
       const double gjj = sW[k + j + j * m];
       const double thr = fmax(thr_abs, a.eta * gjj);
-      if (!(d > thr)) continue;  // deflated column (also catches NaN)
+      if (!(d > thr)) continue;  // deflated column (also catches NaN); uniform across lanes
       // pivot sqrt(d) and its inverse from one reciprocal square root (no fp64 division on
       // the latency-bound critical path)
       const double inv = rsqrt(d);
-      const double njj = d * inv;
-      if (lane == 0) { sN[r + j * kSMax] = njj; sPiv[r] = j; sInv[r] = inv; }
-      if (lane > j && lane < s) sN[r + lane * kSMax] = sS[j + lane * kSMax] * inv;
+      const double nx = (lane > j && lane < s) ? Srow[j * kSMax] * inv : 0.0;  // N(r, lane)
+      if (lane == 0) { sN[r + j * kSMax] = d * inv; sPiv[r] = j; sInv[r] = inv; }
+      if (lane > j && lane < s) sN[r + lane * kSMax] = nx;
       __syncwarp();
-      for (int e = lane; e < s * s; e += 32) {
-        const int x = e % s, y = e / s;
-        if (x > j && y > j) sS[x + y * kSMax] -= sN[r + x * kSMax] * sN[r + y * kSMax];
-      }
+      if (lane > j && lane < s)
+        for (int y = j + 1; y < s; ++y) Srow[y * kSMax] = fma(-nx, sN[r + y * kSMax], Srow[y * kSMax]);
       __syncwarp();
       ++r;
     }

@@ -101,6 +101,11 @@ struct Ctx {
   double *Pf = nullptr, *Nf = nullptr;
   int* ints = nullptr;      // [0] t1 [1] t2 [2] tf [3] defl1 [4] defl2 [16..] piv1 [32..] piv2
   int* h_ints = nullptr;    // pinned host mirror
+  int* d_hints = nullptr;   // device view of h_ints (mapped pinned memory: kernels write t directly)
+  // the caller's device P / N of the current call (nullptr: host or absent); a kernel that writes
+  // them itself sets outs_written so the call enqueues no output copies
+  double* outP = nullptr; int outldp = 0; double* outN = nullptr; int outldn = 0;
+  bool outs_written = false;
   double* stageX = nullptr;  // n x s_max staging for host X
   double* stageU = nullptr;  // n x s_max staging for host U / internal U1
   double* stageC = nullptr;  // cap x 16 staging for host C
@@ -600,6 +605,7 @@ struct BasisView {
   int k = -1;          // basis columns (-1: the handle's k)
   bool local = false;  // this rank alone: no cross-rank exchange, deflation only of non-positive
                        // pivots (a TSQR local problem never drops columns, reading R4)
+  bool user_out = false;  // the call's own solve: kernels may write the caller's P / N directly
 };
 
 int gram_and_exchange(Ctx* h, const BasisView& bv, int k, int s, const double* X, int64_t ldx, const double** Wsum,
@@ -642,8 +648,9 @@ int run_small(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, 
   const int64_t n = bv.n;
   const int k = bv.k >= 0 ? bv.k : h->k;
   if (n > nmax) return PQR_EPLAN;
-  // rows per CTA: at least 256 (fewer partials to sum), at most what the shared memory holds
+  // rows per CTA (even): at least 256 (fewer partials to sum), at most what the shared memory holds
   int R = (int)std::max<int64_t>(256, (n + h->sms - 1) / h->sms);
+  R += R & 1;
   const size_t budget = 232448 - 28 * 1024;  // minus factor_body's static shared memory
   while (R > 16 && small_smem(R, k, s) > budget) R -= 16;
   const int G = (int)((n + R - 1) / R);
@@ -662,19 +669,25 @@ int run_small(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int s, 
   const int m = k + s;
   SmallArgs a{};
   a.Q = bv.Q; a.ldq = bv.ldq; a.X = X; a.ldx = ldx; a.n = n; a.k = k; a.s = s; a.R = R;
+  a.vec = ((k == 0 || (aligned16(bv.Q) && (bv.ldq & 1) == 0)) && aligned16(X) && (ldx & 1) == 0) ? 1 : 0;
   a.single = single ? 1 : 0; a.tol2 = tol2; a.eta = eta;
   a.U = Ud; a.ldu = ldud; a.U2 = Uappend; a.ldu2 = h->ld;
   a.part1 = h->partials; a.part2 = h->partials + (size_t)h->sms * m * s;
-  a.bar = h->ticket + 1;
+  a.bar = h->ticket + 1;  // zeroed at pqr_create, reset by every launch
   a.Pf = h->Pf; a.ldp = std::max(1, k); a.Nf = h->Nf; a.ints = h->ints;
-  CUDA_TRY(cudaMemsetAsync(h->ticket + 1, 0, sizeof(unsigned int), h->stream));
+  a.hints = h->d_hints;
+  if (bv.user_out) {
+    a.Pout = k > 0 ? h->outP : nullptr; a.ldpo = h->outldp;
+    a.Nout = h->outN; a.ldno = h->outldn;
+  }
   {
     PROF(h, PQR_K_UPDATE_GRAM);
     void* args[] = {&a};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cholqr2_small, G, kSmallThreads, args, smem, h->stream));
   }
   ++h->st.kernel_launches;
-  CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
+  if (!h->d_hints) CUDA_TRY(cudaMemcpyAsync(h->h_ints, h->ints, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
+  if (bv.user_out) h->outs_written = true;
   return PQR_OK;
 }
 
@@ -866,6 +879,10 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   if ((rc = dalloc(&h->M1, (size_t)h->cap * sm)) || (rc = dalloc(&h->M2, (size_t)h->cap * sm))) return fail(rc);
   if ((rc = dalloc(&h->ints, 64))) return fail(rc);
   if (cudaMallocHost(&h->h_ints, 64 * sizeof(int)) != cudaSuccess) return fail(PQR_ENOMEM);
+  if (cudaHostGetDevicePointer((void**)&h->d_hints, h->h_ints, 0) != cudaSuccess) {
+    cudaGetLastError();  // not mapped: t comes back with a copy
+    h->d_hints = nullptr;
+  }
   if (cudaMemsetAsync(h->ticket, 0, 4 * sizeof(unsigned int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
   if (cudaMemsetAsync(h->ints, 0, 64 * sizeof(int), h->stream) != cudaSuccess) return fail(PQR_ECUDA);
 
@@ -1038,16 +1055,23 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
       CUDA_TRY(cudaStreamWaitEvent(h->gstream, h->gev, 0));
       h->stream = h->gstream;
     }
-    capturing = h->stream && cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    capturing = h->stream && !wy_trace_buf() && cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (!capturing) cudaGetLastError();
   }
   h->gcand = graphable ? key : GraphKey{};
   const int64_t launches0 = h->st.kernel_launches;
   auto enqueue = [&]() -> int {
     int rc;
+    h->outP = (P && k > 0 && !is_host_ptr(P)) ? P : nullptr;
+    h->outldp = ldp;
+    h->outN = (N && !is_host_ptr(N)) ? N : nullptr;
+    h->outldn = ldn;
+    h->outs_written = false;
     if (h->cfg.variant == PQR_CHOLQR2) {
       double* Uapp = (append && Ud != h->basis + (int64_t)k * h->ld) ? h->basis + (int64_t)k * h->ld : nullptr;
-      rc = cholqr2_solve(h, BasisView{h->basis, h->ld, n}, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
+      BasisView bv{h->basis, h->ld, n};
+      bv.user_out = true;
+      rc = cholqr2_solve(h, bv, Xd, ldxd, s, flags, Ud, ldud, Uapp, &tt, tau);
     } else {
       rc = tsqr_solve(h, Xd, ldxd, s, flags, Ud, ldud, append, &tt);
     }
@@ -1058,10 +1082,10 @@ int pqr_project_normalize(pqr_handle hh, const double* X, int64_t ldx, int s, un
       CUDA_TRY(cudaMemcpy2DAsync(U, ldu * sizeof(double), Ud, ldud * sizeof(double), n * sizeof(double), s,
                                  cudaMemcpyDefault, h->stream));
     }
-    if (P && k > 0)
+    if (P && k > 0 && !(h->outs_written && h->outP == P))
       CUDA_TRY(cudaMemcpy2DAsync(P, (size_t)ldp * sizeof(double), h->Pf, (size_t)std::max(1, k) * sizeof(double),
                                  (size_t)k * sizeof(double), s, cudaMemcpyDefault, h->stream));
-    if (N)
+    if (N && !(h->outs_written && h->outN == N))
       CUDA_TRY(cudaMemcpy2DAsync(N, (size_t)ldn * sizeof(double), h->Nf, (size_t)kSMax * sizeof(double),
                                  (size_t)s * sizeof(double), s, cudaMemcpyDefault, h->stream));
     return PQR_OK;
