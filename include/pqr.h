@@ -82,6 +82,20 @@ typedef enum { PQR_CHOLQR2 = 0, PQR_TSQR = 1 } pqr_variant;
  *                    Exists for the stability experiment of PAPER.md:L1274-1291 (fig:heatmap). */
 #define PQR_LOCAL_HH   0
 #define PQR_LOCAL_PIP2 1
+/* How the small blocks cross GPUs (nranks > 1 with nccl_id, or PQR_FORCE_NCCL=1):
+ *   PQR_EXCHANGE_COLLECTIVE — ncclAllGather on the handle's stream between the library's kernels
+ *                             (kernel -> NCCL kernel -> kernel);
+ *   PQR_EXCHANGE_LSA        — the NCCL device API: a kernel stores the rank's block straight into
+ *                             every peer's slot of a symmetric NCCL window over NVLink and meets
+ *                             the peers at an LSA barrier; for CholQR2 this is done by the factor
+ *                             kernel itself (no separate exchange launch).  Needs every rank in one
+ *                             NVLink (LSA) domain and symmetric-memory support; pqr_create returns
+ *                             PQR_ENCCL when either is missing.  (PAPER.md:L1160-1166, L1546-1552:
+ *                             the reduction as a stateful in-network step.)
+ *   PQR_EXCHANGE_AUTO (0)   — COLLECTIVE, unless PQR_EXCHANGE=lsa is set in the environment. */
+#define PQR_EXCHANGE_AUTO       0
+#define PQR_EXCHANGE_COLLECTIVE 1
+#define PQR_EXCHANGE_LSA        2
 
 /* flags of pqr_project_normalize */
 #define PQR_NO_APPEND     1u  /* do not append U to the basis (k unchanged)          */
@@ -106,6 +120,8 @@ typedef struct {
                            pqr_vgroup_create); nccl_id is then ignored.                     */
   int reduction;        /* PQR_TSQR: PQR_REDUCTION_HH (default) or PQR_REDUCTION_PIP2          */
   int local;            /* PQR_TSQR: PQR_LOCAL_HH (default) or PQR_LOCAL_PIP2                  */
+  int exchange;         /* PQR_EXCHANGE_AUTO / _COLLECTIVE / _LSA (NCCL ranks only; ignored for
+                           one rank without PQR_FORCE_NCCL and for virtual groups)            */
 } pqr_config;
 
 /* Create a handle owning the basis (capacity k_max + s_max columns), its workspaces
@@ -153,6 +169,8 @@ typedef struct {
   int64_t kernel_launches;   /* kernels launched by the library (all calls)           */
   int block_rows;            /* TSQR leaf block rows in use (0 for CHOLQR2)           */
   int tree_levels;           /* TSQR on-GPU tree levels (0 for CHOLQR2)               */
+  int exchange;              /* 0 none (one rank), 1 NCCL collective, 2 NCCL device API
+                                (LSA), 3 virtual-rank group                              */
 } pqr_stats;
 int pqr_get_stats(pqr_handle h, pqr_stats* st);
 

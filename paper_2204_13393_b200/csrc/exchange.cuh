@@ -27,10 +27,17 @@
 
 namespace pqr {
 
+struct LsaArgs;  // lsa_exchange.cuh
+
+enum { kXNccl = 1, kXLsa = 2, kXVirtual = 3 };  // pqr_stats.exchange
+
 struct Exchange {
   int rank = 0, nranks = 1;
+  int kind = 0;
   int64_t calls = 0, bytes = 0;
   virtual ~Exchange() {}
+  // NCCL device-API exchange: the arguments a kernel needs to exchange by itself (else nullptr)
+  virtual const LsaArgs* lsa() const { return nullptr; }
   // recv[j*count, (j+1)*count) = rank j's send[0, count) for every rank j, ordered on st
   // (send must not be overwritten by later work of this rank before every rank has read
   // it: both implementations guarantee that on the stream).  Returns 0 or a PQR_E* code.
@@ -39,6 +46,7 @@ struct Exchange {
 
 struct NcclExchange : Exchange {
   ncclComm_t comm = nullptr;
+  NcclExchange() { kind = kXNccl; }
   ~NcclExchange() override {
     if (comm) ncclCommDestroy(comm);
   }
@@ -102,6 +110,7 @@ struct VirtualGroup {
 struct VirtualExchange : Exchange {
   VirtualGroup* g = nullptr;
   cudaEvent_t ready = nullptr, done = nullptr;
+  VirtualExchange() { kind = kXVirtual; }
   ~VirtualExchange() override {
     if (g) g->leave();
   }

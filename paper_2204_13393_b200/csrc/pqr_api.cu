@@ -21,6 +21,7 @@
 #include "small_kernels.cuh"
 #include "support_kernels.cuh"
 #include "exchange.cuh"
+#include "lsa_exchange.cuh"
 
 using namespace pqr;
 
@@ -487,8 +488,14 @@ int run_update(int64_t n, int k, const double* Q, int64_t ldq, int sx, const dou
   return PQR_OK;
 }
 
-int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches) {
-  k_factor<<<1, kThreads, 0, st>>>(a);
+// nparts < 0: the Grams cross the ranks inside the factor kernel (NCCL device API, lsa)
+int run_factor(const FactorArgs& a, cudaStream_t st, int64_t* launches, const LsaArgs* lsa = nullptr) {
+  if (a.nparts < 0) {
+    if (!lsa) return PQR_EARG;
+    k_factor_lsa<<<1, kThreads, 0, st>>>(a, *lsa);
+  } else {
+    k_factor<<<1, kThreads, 0, st>>>(a);
+  }
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -626,7 +633,13 @@ int gram_and_exchange(Ctx* h, const BasisView& bv, int k, int s, const double* X
 
 // (nranks > 1) allgather this rank's Gram so every rank sums all ranks' in rank order
 int exchange(Ctx* h, int m, int s, const double** Wsum, int* nparts) {
-  if (h->xc) {
+  if (h->xc && h->xc->lsa()) {
+    // device-API exchange: k_factor_lsa stores this Gram into every peer's window itself
+    h->st.collectives += 1;
+    h->st.collective_bytes += (int64_t)m * s * 8;
+    *Wsum = h->Wloc;
+    *nparts = -1;
+  } else if (h->xc) {
     PROF(h, PQR_K_NCCL);
     TRY(h->xc->allgather(h->Wloc, h->Wall, (size_t)m * s, h->stream));
     h->st.collectives += 1;
@@ -735,7 +748,7 @@ int cholqr2_solve(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int
   f.t_out = d_t1; f.piv_out = h->ints + 16; f.deflated = d_def;
   {
     PROF(h, PQR_K_FACTOR);
-    TRY(run_factor(f, h->stream, &h->st.kernel_launches));
+    TRY(run_factor(f, h->stream, &h->st.kernel_launches, h->xc ? h->xc->lsa() : nullptr));
   }
   bool fused = false;
   if (!single) {
@@ -775,7 +788,7 @@ int cholqr2_solve(Ctx* h, const BasisView& bv, const double* X, int64_t ldx, int
     f2.Pf = h->Pf; f2.ldpf = std::max(1, k); f2.Nf = h->Nf; f2.ldnf = kSMax; f2.tf = h->ints + 2;
     {
       PROF(h, PQR_K_FACTOR);
-      TRY(run_factor(f2, h->stream, &h->st.kernel_launches));
+      TRY(run_factor(f2, h->stream, &h->st.kernel_launches, h->xc ? h->xc->lsa() : nullptr));
     }
     if (h->hp.nch > 0) {
       // host U: the final pass per chunk, each chunk's rows copied out behind it
@@ -903,7 +916,12 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
     } else if (ncclGetUniqueId(&id) != ncclSuccess) {
       return fail(PQR_ENCCL);
     }
-    auto* nx = new NcclExchange();
+    if (cfg->exchange != PQR_EXCHANGE_AUTO && cfg->exchange != PQR_EXCHANGE_COLLECTIVE &&
+        cfg->exchange != PQR_EXCHANGE_LSA)
+      return fail(PQR_EARG);
+    static const bool env_lsa = getenv("PQR_EXCHANGE") && strcmp(getenv("PQR_EXCHANGE"), "lsa") == 0;
+    const bool use_lsa = cfg->exchange == PQR_EXCHANGE_LSA || (cfg->exchange == PQR_EXCHANGE_AUTO && env_lsa);
+    NcclExchange* nx = use_lsa ? new LsaExchange() : new NcclExchange();
     nx->rank = cfg->rank;
     nx->nranks = cfg->nranks;
     h->xc = nx;
@@ -913,6 +931,10 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
       nx->comm = nullptr;
       return fail(PQR_ENCCL);
     }
+    // window slots hold the largest block either variant sends: (k_max + s_max) x s_max
+    if (use_lsa)
+      if (const int e = static_cast<LsaExchange*>(nx)->setup((int64_t)h->cap * cfg->s_max))
+        return fail(e == -7 ? PQR_ENOMEM : (e == -5 ? PQR_ECUDA : PQR_ENCCL));
   }
 
   // host Q is staged through a temporary device copy
@@ -1209,6 +1231,7 @@ int pqr_get_stats(pqr_handle hh, pqr_stats* st) {
   Ctx* h = reinterpret_cast<Ctx*>(hh);
   if (!h || !st) return PQR_EARG;
   *st = h->st;
+  st->exchange = h->xc ? h->xc->kind : 0;
   return PQR_OK;
 }
 

@@ -25,6 +25,8 @@ PQR_REDUCTION_HH, PQR_REDUCTION_PIP2 = 0, 1
 REDUCTIONS = {"hh": PQR_REDUCTION_HH, "pip2": PQR_REDUCTION_PIP2}
 PQR_LOCAL_HH, PQR_LOCAL_PIP2 = 0, 1
 LOCALS = {"hh": PQR_LOCAL_HH, "pip2": PQR_LOCAL_PIP2}
+PQR_EXCHANGE_AUTO, PQR_EXCHANGE_COLLECTIVE, PQR_EXCHANGE_LSA = 0, 1, 2
+EXCHANGES = {"auto": PQR_EXCHANGE_AUTO, "collective": PQR_EXCHANGE_COLLECTIVE, "lsa": PQR_EXCHANGE_LSA}
 
 
 class PQRError(RuntimeError):
@@ -39,7 +41,7 @@ class pqr_config(ctypes.Structure):
         ("variant", ctypes.c_int), ("defl_tol", ctypes.c_double), ("gram_eta", ctypes.c_double),
         ("block_rows", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
         ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("vgroup", ctypes.c_void_p),
-        ("reduction", ctypes.c_int), ("local", ctypes.c_int),
+        ("reduction", ctypes.c_int), ("local", ctypes.c_int), ("exchange", ctypes.c_int),
     ]
 
 
@@ -48,6 +50,7 @@ class pqr_stats(ctypes.Structure):
         ("k", ctypes.c_int), ("last_t", ctypes.c_int), ("calls", ctypes.c_int64),
         ("collectives", ctypes.c_int64), ("collective_bytes", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64), ("block_rows", ctypes.c_int), ("tree_levels", ctypes.c_int),
+        ("exchange", ctypes.c_int),
     ]
 
 
@@ -161,7 +164,7 @@ def _stream_ptr(stream):
 # ---------------------------------------------------------------------------
 def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0.0, gram_eta=0.0, block_rows=0,
                stream=None, rank=0, nranks=1, nccl_id: bytes | None = None, vgroup=None, reduction="hh",
-               local="hh"):
+               local="hh", exchange="auto"):
     cfg = pqr_config()
     cfg.n_local = int(n_local)
     cfg.k_max = int(k_max)
@@ -176,6 +179,7 @@ def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0
     cfg.vgroup = vgroup.value if isinstance(vgroup, ctypes.c_void_p) else vgroup
     cfg.reduction = REDUCTIONS[reduction] if isinstance(reduction, str) else int(reduction)
     cfg.local = LOCALS[local] if isinstance(local, str) else int(local)
+    cfg.exchange = EXCHANGES[exchange] if isinstance(exchange, str) else int(exchange)
     idbuf = None
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)

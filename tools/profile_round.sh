@@ -7,7 +7,7 @@ timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_
 timeout 300 $B > gpurun_out/${TAG}_bench_short.json 2>&1 || exit 1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wy_up -s 119 -c 1 -o gpurun_out/${TAG}_wy_up python bench.py --variant tsqr --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${TAG}_wy_up.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_update_gram|k_gram_cpa|k_update_cpa" -s 3 -c 3 -o gpurun_out/${TAG}_cholqr python bench.py --variant cholqr2 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${TAG}_cholqr.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_stream2|k_gram_cpa|k_update_cpa" -s 3 -c 3 -o gpurun_out/${TAG}_cholqr python bench.py --variant cholqr2 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${TAG}_cholqr.log 2>&1
 # leaf stage-2 launch: the first k_wy_down launch of the timed step that runs > 3 ms
 T="python bench.py --variant tsqr --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:k_wy_down $T 2>/dev/null > gpurun_out/${TAG}_down_list.csv
