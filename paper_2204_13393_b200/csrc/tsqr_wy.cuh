@@ -43,6 +43,15 @@ namespace pqr {
 // 16 consumer warps per CTA, as one group or as two groups of 8 on alternate blocks (see the
 // kernels at the end); UW below is per-warp units for the group's warp count, the host plans
 // in 16-warp units.
+#ifndef PQR_WY_ONEBAR8
+#define PQR_WY_ONEBAR8 1
+#endif
+#ifndef PQR_WY_ONEBAR16
+#define PQR_WY_ONEBAR16 1
+#endif
+#ifndef PQR_WY_ROT16
+#define PQR_WY_ROT16 1  // 16-column tail: rotated register file (0: select-chain loop)
+#endif
 constexpr int kWyWarps = 16;                     // consumer warps per CTA
 constexpr int kWyThreads = 32 * kWyWarps;        // consumer threads
 constexpr int kWyLaunch = kWyThreads + 128;      // + one producer warpgroup (one working lane)
@@ -90,7 +99,7 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
 // per-group scratch (doubles) of a level kernel with NW consumer warps per group:
 // partials (NW + 1) E, Z (E), Householder-round buffers, diag, T scratch, round coefficients
 PQR_HOST_DEV constexpr int wy_group_scratch(int NW, int E) {
-  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 64;
+  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 64 + 16 * NW;
 }
 // shared-memory bytes of a level kernel (host and device agree on this layout)
 inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf, int NW, int NG) {
@@ -126,6 +135,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   double* diagv = hred + 2 * (NW * kWyHS + 16);  // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
   double* hfc = tsc + 512;                 // 2 x 32: Householder-round coefficients (by round parity)
+  double* hupd = hfc + 64;                 // NW x 16: per-warp round coefficients (16-column tail)
   int4* pans = reinterpret_cast<int4*>(ring + (size_t)nbuf * SS + NG * GS);
   uint64_t* full = reinterpret_cast<uint64_t*>(pans + L.cap + 2);
   uint64_t* empty = full + nbuf;
@@ -518,6 +528,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     //   v_c' . v_c by the same formula for c' < c (column c of V^T V, for T).
     constexpr int RPL = UW / 2;   // rows per lane in the row layout
     constexpr int S8 = 8 * NT;    // columns per row
+    // one barrier per Householder round (every warp forms the scalars) or two (warp 0 forms them)
+    constexpr bool ONEBAR = S8 == 8 ? PQR_WY_ONEBAR8 : PQR_WY_ONEBAR16;
     double xr[RPL][S8];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -554,6 +566,74 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       rowk[e] = 16 * (warp * UW + (sg >> 2)) + 4 * q + (sg & 3);
     }
     double* Gs = tsc;  // strict upper part of V^T V (ld 16), column c written in round c by tid 0
+    // Round scalars, formed by every warp from the NW warp partials of hb (the same fixed summation
+    // order in every warp and lane: bitwise-identical values), so a round needs one barrier:
+    //   lambda, sigma = -sgn(u0), v's scale inv = 1/sqrt(2 lambda (lambda + |u0|)), wr = u0 - sigma*lambda,
+    //   fvc[c'] = 2 v . x_c' = 2 inv (D_c' - sigma*lambda x_c'[r]) (c' > c: update coefficient;
+    //   c' < c: twice column c of V^T V, recorded for T by warp 0).  hb is double-buffered by round
+    //   parity: a warp's reads of round c precede its arrival at round c + 1's barrier.
+    auto round_scalars = [&](int c, const double* hb, double (&fvc)[S8], double& inv, double& wr) {
+      constexpr int NP = 32 / S8, WPP = NW / NP;  // lane groups, warps per group
+      const int v = lane & (S8 - 1), part = lane / S8;
+      const double* hv = hb + part * WPP * kWyHS + v;
+      double tot = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
+#pragma unroll
+      for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
+      const double lam2 = __shfl_sync(0xffffffffu, tot, c);
+      const double u0 = hb[NW * kWyHS + c];
+      const double lam = sqrt(lam2);
+      const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
+      const double diag = sigma * lam;
+      const double nv2 = 2.0 * lam * (lam + fabs(u0));
+      inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
+      wr = u0 - diag;
+      const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[NW * kWyHS + v]);
+#pragma unroll
+      for (int cc = 0; cc < S8; ++cc) fvc[cc] = __shfl_sync(0xffffffffu, fv, cc);
+      if (warp == 0) {
+        if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
+        if (lane == 0) diagv[c] = diag;
+      }
+    };
+    // Two-barrier form: warp 0 alone forms the scalars and publishes them (hfc, by round parity)
+    // behind a second barrier.
+    auto round_scalars_w0 = [&](int c, const double* hb, double (&fvc)[S8], double& inv, double& wr) {
+      double* hf = hfc + (c & 1) * 32;  // [0, S8): coefficients; S8: inv; S8+1: u0 - sigma*lambda
+      if (warp == 0) {
+        constexpr int NP = 32 / S8, WPP = NW / NP;
+        const int v = lane & (S8 - 1), part = lane / S8;
+        const double* hv = hb + part * WPP * kWyHS + v;
+        double tot = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
+#pragma unroll
+        for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
+        const double lam2 = __shfl_sync(0xffffffffu, tot, c);
+        const double u0 = hb[NW * kWyHS + c];
+        const double lam = sqrt(lam2);
+        const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;
+        const double diag = sigma * lam;
+        const double nv2 = 2.0 * lam * (lam + fabs(u0));
+        const double iv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;
+        const double fv = v == c ? 0.0 : 2.0 * iv * (tot - diag * hb[NW * kWyHS + v]);
+        if (lane < S8) {
+          hf[lane] = fv;
+          if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
+        }
+        if (lane == 0) {
+          hf[S8] = iv;
+          hf[S8 + 1] = u0 - diag;
+          diagv[c] = diag;
+        }
+      }
+      cbar();
+      inv = hf[S8];
+      wr = hf[S8 + 1];
+#pragma unroll
+      for (int cc = 0; cc < S8; ++cc) fvc[cc] = hf[cc];
+    };
     WY_TR(10);
     if constexpr (S8 == 8) {
 #pragma unroll
@@ -594,53 +674,131 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int cc = 0; cc < S8; ++cc) hb[NW * kWyHS + cc] = xr[e][cc];
         }
       WY_TR(11);
-      cbar();
+      cbar();  // the round's only barrier: partials and pivot row complete
       WY_TR(12);
-      // Warp 0 alone sums the 16 warp partials, forms the reflector scalars (one sqrt/rsqrt
-      // chain per CTA) and the update coefficients, and publishes them behind a second barrier
-      // (cheaper than every warp reducing and broadcasting the totals itself).
-      double* hf = hfc + (c & 1) * 32;  // [0, S8): coefficients; S8: inv; S8+1: u0 - sigma*lambda
-      if (warp == 0) {
-        constexpr int NP = 32 / S8, WPP = NW / NP;  // lane groups, warps per group
-        const int v = lane & (S8 - 1), part = lane / S8;
-        const double* hv = hb + part * WPP * kWyHS + v;
-        double tot = 0.0;
-#pragma unroll
-        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
-#pragma unroll
-        for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
-        const double lam2 = __shfl_sync(0xffffffffu, tot, c);
-        const double u0 = hb[NW * kWyHS + c];
-        const double lam = sqrt(lam2);
-        const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
-        const double diag = sigma * lam;
-        const double nv2 = 2.0 * lam * (lam + fabs(u0));
-        const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
-        // v . x_v (v > c: update coefficient / 2) and v_v . v_c (v < c: column c of V^T V)
-        const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[NW * kWyHS + v]);
-        if (lane < S8) {
-          hf[lane] = fv;
-          if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
-        }
-        if (lane == 0) {
-          hf[S8] = inv;
-          hf[S8 + 1] = u0 - diag;
-          diagv[c] = diag;
-        }
+      double fvc[S8];
+      double inv, wr;
+      if constexpr (ONEBAR) {
+        round_scalars(c, hb, fvc, inv, wr);
+      } else {
+        round_scalars_w0(c, hb, fvc, inv, wr);
       }
-      WY_TR(14);
-      cbar();
-      WY_TR(15);
-      const double inv = hf[S8], wr = hf[S8 + 1];
       WY_TR(13);
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
         if (rowk[e] >= r) {
           const double vv = (rowk[e] == r ? wr : xr[e][c]) * inv;
 #pragma unroll
-          for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-hf[cc], vv, xr[e][cc]);
+          for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-fvc[cc], vv, xr[e][cc]);
           xr[e][c] = vv;
         }
+    }
+    } else {
+    if constexpr (PQR_WY_ROT16) {
+    // 16 columns, rotated register file: entering a group of RU rounds with base c0, xr[e][j] holds
+    // column (c0 + j) mod 16, so round c = c0 + cj pivots on the compile-time index cj and every
+    // register index is static (no select chains, no per-column predicates); the group ends by
+    // rotating the columns by RU (16 rounds: back to identity).  Coefficients of finished columns
+    // are zero, so the update is one unpredicated FMA per element (an exact no-op there).
+    constexpr int RU = 4;
+    double* wup = hupd + warp * 16;  // this warp's update coefficients of the round
+#pragma unroll 1
+    for (int c0 = 0; c0 < S8; c0 += RU) {
+#pragma unroll
+      for (int cj = 0; cj < RU; ++cj) {
+        const int c = c0 + cj;
+        if (c < s) {
+          const int r = C + c;
+          double D[S8];
+#pragma unroll
+          for (int j = 0; j < S8; ++j) D[j] = 0.0;
+#pragma unroll
+          for (int e = 0; e < RPL; ++e)
+            if (rowk[e] >= r) {
+#pragma unroll
+              for (int j = 0; j < S8; ++j) D[j] = fma(xr[e][cj], xr[e][j], D[j]);
+            }
+#pragma unroll
+          for (int mb = 16, w = S8; w > 1; mb >>= 1, w >>= 1) {
+            const bool up = (lane & mb) != 0;
+#pragma unroll
+            for (int j = 0; j < w / 2; ++j) {
+              const double send = up ? D[j] : D[j + w / 2];
+              const double keep = up ? D[j + w / 2] : D[j];
+              D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
+            }
+          }
+          D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
+          const int vi = (lane >> 1) & (S8 - 1);  // rotated index of the value this lane holds
+          double* hb = hred + hpar * (NW * kWyHS + 16);
+          hpar ^= 1;
+          if ((lane & 1) == 0) hb[warp * kWyHS + vi] = D[0];
+#pragma unroll
+          for (int e = 0; e < RPL; ++e)
+            if (rowk[e] == r) {
+#pragma unroll
+              for (int j = 0; j < S8; ++j) hb[NW * kWyHS + j] = xr[e][j];
+            }
+          WY_TR(11);
+          cbar();  // the round's only barrier
+          WY_TR(12);
+          double inv, wr;
+          {
+            // every warp sums the NW partials of its value j = lane & 15 (fixed order) and forms the
+            // scalars; column (c0 + j) mod 16: > c update target, < c finished (column c of V^T V)
+            constexpr int WPP = NW / 2;
+            const int j = lane & 15, part = lane >> 4;
+            const double* hv = hb + part * WPP * kWyHS + j;
+            double tot = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
+            tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+            const double lam2 = __shfl_sync(0xffffffffu, tot, cj);
+            const double u0 = hb[NW * kWyHS + cj];
+            const double lam = sqrt(lam2);
+            const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;  // sigma = -sgn(u0), sgn(0) = +1
+            const double diag = sigma * lam;
+            const double nv2 = 2.0 * lam * (lam + fabs(u0));
+            inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
+            wr = u0 - diag;
+            const double fv = 2.0 * inv * (tot - diag * hb[NW * kWyHS + j]);
+            const int col = (c0 + j) & 15;
+            if (lane < 16) wup[j] = col > c ? fv : 0.0;
+            if (warp == 0) {
+              if (lane < 16 && col < c) Gs[col + 16 * c] = 0.5 * fv;
+              if (lane == 0) diagv[c] = diag;
+            }
+            __syncwarp();
+          }
+          WY_TR(13);
+          double up[S8];
+#pragma unroll
+          for (int j = 0; j < S8; j += 2) {
+            const double2 u2 = *reinterpret_cast<const double2*>(wup + j);
+            up[j] = u2.x;
+            up[j + 1] = u2.y;
+          }
+#pragma unroll
+          for (int e = 0; e < RPL; ++e)
+            if (rowk[e] >= r) {
+              const double vv = (rowk[e] == r ? wr : xr[e][cj]) * inv;
+#pragma unroll
+              for (int j = 0; j < S8; ++j)
+                if (j != cj) xr[e][j] = fma(-up[j], vv, xr[e][j]);
+              xr[e][cj] = vv;
+            }
+          __syncwarp();  // wup is rewritten next round
+        }
+      }
+      // rotate by RU: column (c0 + RU + j) mod 16 to index j
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) {
+        double tmp[S8];
+#pragma unroll
+        for (int j = 0; j < S8; ++j) tmp[j] = xr[e][(j + RU) & (S8 - 1)];
+#pragma unroll
+        for (int j = 0; j < S8; ++j) xr[e][j] = tmp[j];
+      }
     }
     } else {
     // 16 columns: the rounds stay a loop (fully unrolled they overflow the instruction cache);
@@ -690,40 +848,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int cc = 0; cc < S8; ++cc) hb[NW * kWyHS + cc] = xr[e][cc];
         }
       WY_TR(11);
-      cbar();
+      cbar();  // the round's only barrier
       WY_TR(12);
-      double* hf = hfc + (c & 1) * 32;
-      if (warp == 0) {
-        constexpr int NP = 32 / S8, WPP = NW / NP;
-        const int v = lane & (S8 - 1), part = lane / S8;
-        const double* hv = hb + part * WPP * kWyHS + v;
-        double tot = 0.0;
-#pragma unroll
-        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
-#pragma unroll
-        for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
-        const double lam2 = __shfl_sync(0xffffffffu, tot, c);
-        const double u0 = hb[NW * kWyHS + c];
-        const double lam = sqrt(lam2);
-        const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;
-        const double diag = sigma * lam;
-        const double nv2 = 2.0 * lam * (lam + fabs(u0));
-        const double inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;
-        const double fv = v == c ? 0.0 : 2.0 * inv * (tot - diag * hb[NW * kWyHS + v]);
-        if (lane < S8) {
-          hf[lane] = fv;
-          if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
-        }
-        if (lane == 0) {
-          hf[S8] = inv;
-          hf[S8 + 1] = u0 - diag;
-          diagv[c] = diag;
-        }
+      double fvc[S8];
+      double inv, wr;
+      if constexpr (ONEBAR) {
+        round_scalars(c, hb, fvc, inv, wr);
+      } else {
+        round_scalars_w0(c, hb, fvc, inv, wr);
       }
-      WY_TR(14);
-      cbar();
-      WY_TR(15);
-      const double inv = hf[S8], wr = hf[S8 + 1];
       WY_TR(13);
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
@@ -731,12 +864,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           const double vv = (rowk[e] == r ? wr : xc[e]) * inv;
 #pragma unroll
           for (int cc = 0; cc < S8; ++cc) {
-            if (cc > c) xr[e][cc] = fma(-hf[cc], vv, xr[e][cc]);
+            if (cc > c) xr[e][cc] = fma(-fvc[cc], vv, xr[e][cc]);
             else if (cc == c) xr[e][cc] = vv;
           }
         }
     }
     }
+    }
+    // sigma*lambda (diagv) of the last round is read by every warp below
+    cbar();
     WY_TR(7);
     // ---------------- T of the new panel: T^{-1} = I/2 + striu(V^T V) (warp 0) ----------------
     __syncwarp();
