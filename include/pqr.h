@@ -93,6 +93,22 @@ typedef enum { PQR_CHOLQR2 = 0, PQR_TSQR = 1 } pqr_variant;
  *                             PQR_ENCCL when either is missing.  (PAPER.md:L1160-1166, L1546-1552:
  *                             the reduction as a stateful in-network step.)
  *   PQR_EXCHANGE_AUTO (0)   — COLLECTIVE, unless PQR_EXCHANGE=lsa is set in the environment. */
+/* PQR_TSQR with PQR_LOCAL_HH: FlatTSPQR chains of leaf blocks (§4.2, Alg. 10, Eqs.
+ * flat_tsqr / flattspqr_q, L815-983; the paper's own on-node choice, fig:architecture L1195-1200):
+ * the GPU's leaf blocks form 2 x (SM count) chains (chain c = blocks c, c + nchain, ...); block i of
+ * a chain solves the stacked problem [Q_i | P_{i-1}; N_{i-1}; X_i] against its reflectors (which
+ * span the chain's carried coordinates and its own rows), so only the chains' last [P; N] blocks
+ * reach the reduction tree (TreeTSPQR over the chains).  Stage 2 walks every chain backwards
+ * (Eq. flattspqr_q).  The result is another locally orthogonal representation of the same basis:
+ * P, N, t and U agree with the pure tree to rounding.
+ *   PQR_CHAINS_AUTO (0) - the library's choice: currently the pure tree (the chained leaf
+ *                         kernels measure slower than the tree levels they remove);
+ *   PQR_CHAINS_OFF      - pure TreeTSPQR (every leaf block's [P; N] goes to the tree);
+ *   PQR_CHAINS_ON       - chains whenever there are more leaf blocks than chains.
+ * The plan is fixed at pqr_create (pqr_stats.leaf_chains reports the chain count, 0 = none). */
+#define PQR_CHAINS_AUTO 0
+#define PQR_CHAINS_OFF  1
+#define PQR_CHAINS_ON   2
 #define PQR_EXCHANGE_AUTO       0
 #define PQR_EXCHANGE_COLLECTIVE 1
 #define PQR_EXCHANGE_LSA        2
@@ -122,6 +138,7 @@ typedef struct {
   int local;            /* PQR_TSQR: PQR_LOCAL_HH (default) or PQR_LOCAL_PIP2                  */
   int exchange;         /* PQR_EXCHANGE_AUTO / _COLLECTIVE / _LSA (NCCL ranks only; ignored for
                            one rank without PQR_FORCE_NCCL and for virtual groups)            */
+  int chains;           /* PQR_TSQR: PQR_CHAINS_AUTO (default) / _OFF / _ON (FlatTSPQR leaves)  */
 } pqr_config;
 
 /* Create a handle owning the basis (capacity k_max + s_max columns), its workspaces
@@ -171,6 +188,7 @@ typedef struct {
   int tree_levels;           /* TSQR on-GPU tree levels (0 for CHOLQR2)               */
   int exchange;              /* 0 none (one rank), 1 NCCL collective, 2 NCCL device API
                                 (LSA), 3 virtual-rank group                              */
+  int leaf_chains;           /* TSQR FlatTSPQR leaf chains (0: pure tree)                 */
 } pqr_stats;
 int pqr_get_stats(pqr_handle h, pqr_stats* st);
 

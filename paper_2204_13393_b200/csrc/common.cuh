@@ -138,6 +138,23 @@ PQR_DEV void cp_async16(void* dst, const void* src, int src_bytes) {
 PQR_DEV void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
+// cp.async 8-byte global->shared copy (LDGSTS, L1-allocating)
+PQR_DEV void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// L2 evict-last policy (small data re-read long after it is written, under a streaming load)
+PQR_DEV uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+PQR_DEV void st_l2pol(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+PQR_DEV void cp_async8_l2pol(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+               : "memory");
+}
 // as cp_async16 with a 32-bit shared-memory address
 PQR_DEV void cp_async16_s(uint32_t dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");

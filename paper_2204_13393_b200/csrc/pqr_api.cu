@@ -852,6 +852,7 @@ int pqr_create(pqr_handle* out, const pqr_config* cfg, const double* Q, int64_t 
   if (cfg->variant != PQR_CHOLQR2 && cfg->variant != PQR_TSQR) return PQR_EARG;
   if (cfg->reduction != PQR_REDUCTION_HH && cfg->reduction != PQR_REDUCTION_PIP2) return PQR_EARG;
   if (cfg->local != PQR_LOCAL_HH && cfg->local != PQR_LOCAL_PIP2) return PQR_EARG;
+  if (cfg->chains < PQR_CHAINS_AUTO || cfg->chains > PQR_CHAINS_ON) return PQR_EARG;
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return PQR_EARG;
   if (cfg->nranks > 1 && !cfg->nccl_id && !cfg->vgroup) return PQR_EARG;
   if (k > 0 && (!Q || ldq < cfg->n_local)) return PQR_EARG;

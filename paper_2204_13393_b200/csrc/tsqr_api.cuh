@@ -23,6 +23,7 @@ struct TsqrLv {
   double* in = nullptr;      // stage-1 input (node levels / cross level)
   double* dn = nullptr;      // stage-2 output (node levels / cross level)
   bool owns_v = true;
+  bool chained = false;      // the leaf level with FlatTSPQR chains
 };
 
 struct TsqrState {
@@ -42,6 +43,10 @@ struct TsqrState {
   double* Ut = nullptr;      // cap x wmax top coefficients of U (ld cap)
   double* Rt = nullptr;      // cap x cap explicit top basis (ld cap), zero-init
   double* coef = nullptr;    // cap x 16 scratch for basis_apply
+  // FlatTSPQR leaf chains (§4.2 Alg. 10; WyLevel::nchain): nchain chains of leaf blocks,
+  // chain c = blocks c, c + nchain, ...; 0 = every leaf block hands its block to the tree
+  int nchain = 0;
+  double* VC = nullptr;      // carry-area reflector segments (WyLevel::VC): nblocks x cap x (wmax + 2)
 };
 
 // reduction = PIP+ above the GPU tree (pqr.h PQR_REDUCTION_PIP2): no cross-GPU Householder levels
@@ -78,6 +83,23 @@ int groups_for(int64_t nrun, int sms, int UW) {
 template <int UW, int NT, int WM, int NG>
 cudaError_t wy_up_g(const WyLevel& L, const WyPanels& P, int C, int s, int merge, int mtoff, int grid, size_t smem,
                     cudaStream_t st) {
+  if (L.nchain > 0) {  // chained leaf level: two groups (UW <= 4) by construction
+    if constexpr (NG == 2 && UW <= 4) {
+      if constexpr (NT == 1 && WM == 8) {
+        if (merge) {
+          auto f = k_wy_up<UW, NT, WM, true, NG, true>;
+          ensure_smem(f, smem);
+          f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
+          return cudaGetLastError();
+        }
+      }
+      auto f = k_wy_up<UW, NT, WM, false, NG, true>;
+      ensure_smem(f, smem);
+      f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, 0, 0);
+      return cudaGetLastError();
+    }
+    return cudaErrorNotSupported;
+  }
   if constexpr (NT == 1 && WM == 8) {  // panel merges only pair 4-wide panels (s = 4)
     if (merge) {
       auto f = k_wy_up<UW, NT, WM, true, NG>;
@@ -100,6 +122,15 @@ cudaError_t wy_up_t(const WyLevel& L, const WyPanels& P, int C, int s, int merge
 template <int UW, int NT, int WM, int NG>
 cudaError_t wy_down_g(const WyLevel& L, const WyPanels& P, int Call, int t, int ncol, int grid, size_t smem,
                       cudaStream_t st) {
+  if (L.nchain > 0) {  // chained leaf level
+    if constexpr (NG == 2 && UW <= 4) {
+      auto f = k_wy_down<UW, NT, WM, NG, true>;
+      ensure_smem(f, smem);
+      f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
+      return cudaGetLastError();
+    }
+    return cudaErrorNotSupported;
+  }
   auto f = k_wy_down<UW, NT, WM, NG>;
   ensure_smem(f, smem);
   f<<<grid, kWyLaunch, smem, st>>>(L, P, Call, t, ncol);
@@ -148,7 +179,21 @@ WyLevel to_wy(const TsqrState* ts, const TsqrLv& lv) {
   L.V = lv.V; L.ldv = lv.ldv; L.T = lv.T; L.tstride = lv.tstride;
   L.cap = ts->cap; L.RP = lv.RP; L.wmax = ts->wmax; L.nbuf = 2;  // set per kernel kind by the caller
   L.trace = wy_trace_buf();
+  if (lv.chained) {  // the chained leaf level
+    L.nchain = ts->nchain; L.LS = ts->wmax + 2; L.VC = ts->VC;
+  }
   return L;
+}
+// grid and groups of a level launch: a chained level runs nchain / 2 CTAs of two groups (the
+// chain of group g of CTA x is x + g * grid), whatever the number of blocks in the launch
+void wy_shape(const Ctx* h, const TsqrLv& lv, const WyLevel& L, int* grid, int* NG) {
+  if (L.nchain > 0) {
+    *NG = 2;
+    *grid = L.nchain / 2;
+  } else {
+    *NG = groups_for(L.nrun, h->sms, lv.UW);
+    *grid = (int)std::min<int64_t>(L.nrun, h->sms);
+  }
 }
 
 int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* out, int64_t ldo, int np, int C,
@@ -162,10 +207,10 @@ int run_wy_up(Ctx* h, const TsqrLv& lv, const double* X, int64_t ldx, double* ou
   L.ovec = ((ts->cap & 1) == 0 && (ldo & 1) == 0 && aligned16(out)) ? 1 : 0;
   WyPanels P{ts->d_pan, np};
   const int NT = s > 8 ? 2 : 1;
-  const int NG = groups_for(L.nrun, h->sms, lv.UW);
+  int NG, grid;
+  wy_shape(h, lv, L, &grid, &NG);
   L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, NG);
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, NG);
-  const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
 #define UPC(U, N, W) wy_up_t<U, N, W>(L, P, C, s, merge, mtoff, grid, smem, h->stream, NG)
   PQR_WY_SWITCH(lv.UW, NT, ts->wmax, UPC)
@@ -189,10 +234,10 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
   L.yvec = ((ldy & 1) == 0 && aligned16(Y)) ? 1 : 0;
   WyPanels P{pan, np};
   const int NT = ncol > 8 ? 2 : 1;
-  const int NG = groups_for(L.nrun, h->sms, lv.UW);
+  int NG, grid;
+  wy_shape(h, lv, L, &grid, &NG);
   L.nbuf = nbuf_for(lv.RP, ts->wmax, ts->cap, NG);
   const size_t smem = wy_smem(lv.RP, ts->wmax, ts->cap, L.nbuf, NG);
-  const int grid = (int)std::min<int64_t>(L.nrun, h->sms);
   cudaError_t e;
 #define DNC(U, N, W) wy_down_t<U, N, W>(L, P, Call, t, ncol, grid, smem, h->stream, NG)
   PQR_WY_SWITCH(lv.UW, NT, ts->wmax, DNC)
@@ -204,6 +249,14 @@ int run_wy_down(Ctx* h, const TsqrLv& lv, const double* cin, int64_t ldci, doubl
     return PQR_ECUDA;
   }
   return PQR_OK;
+}
+
+// host-pipeline chunk [u0, u1) of leaf units (chained leaves: a unit is one round of nchain blocks)
+// -> blocks [b0, b0 + nrun)
+void leaf_chunk(const TsqrState* ts, int64_t u0, int64_t u1, int64_t* b0, int64_t* nrun) {
+  const int64_t unit = ts->nchain > 0 ? ts->nchain : 1, nb = ts->lv[0].nblocks;
+  *b0 = std::min(nb, u0 * unit);
+  *nrun = std::min(nb, u1 * unit) - *b0;
 }
 
 // Stage 1 over all levels: X (n_local x s) -> Btop ((C+s) x s, ld cap).  Creates s new
@@ -240,7 +293,9 @@ int tsqr_up_sweep(Ctx* h, const double* X, int64_t ldx, int s, int merge = 0, in
       // host X arrives chunk by chunk (leaf blocks are independent in stage 1)
       for (int c = 0; c < h->hp.nch; ++c) {
         TRY(hp_wait_in(h, c));
-        TRY(run_wy_up(h, ts->lv[0], X, ldx, out0, ldo0, np, C, s, merge, mtoff, h->hp.b[c], h->hp.b[c + 1] - h->hp.b[c]));
+        int64_t b0, nrun;
+        leaf_chunk(ts, h->hp.b[c], h->hp.b[c + 1], &b0, &nrun);
+        TRY(run_wy_up(h, ts->lv[0], X, ldx, out0, ldo0, np, C, s, merge, mtoff, b0, nrun));
       }
     } else {
       TRY(run_wy_up(h, ts->lv[0], X, ldx, out0, ldo0, np, C, s, merge, mtoff));
@@ -323,9 +378,13 @@ int tsqr_down_sweep(Ctx* h, int np, int Call, const double* cin, int t, int ncol
   const double* cin0 = ts->nlev >= 1 ? ts->lv[1].dn : root_cin;
   const int64_t ldc0 = ts->nlev >= 1 ? ts->lv[1].rows : root_ld;
   if (pipe && h->hp.nch > 0) {
-    // U leaves for the host chunk by chunk, each copy behind its chunk's stage-2 launch
-    for (int c = 0; c < h->hp.nch; ++c) {
-      TRY(run_wy_down(h, ts->lv[0], cin0, ldc0, Y, ldy, np, Call, t, ncol, pan, h->hp.b[c], h->hp.b[c + 1] - h->hp.b[c]));
+    // U leaves for the host chunk by chunk, each copy behind its chunk's stage-2 launch (chained
+    // leaves: the chains are walked backwards, so the chunks are too)
+    for (int cc = 0; cc < h->hp.nch; ++cc) {
+      const int c = ts->nchain > 0 ? h->hp.nch - 1 - cc : cc;
+      int64_t b0, nrun;
+      leaf_chunk(ts, h->hp.b[c], h->hp.b[c + 1], &b0, &nrun);
+      TRY(run_wy_down(h, ts->lv[0], cin0, ldc0, Y, ldy, np, Call, t, ncol, pan, b0, nrun));
       TRY(hp_d2h_chunk(h, c, Y, ldy, ncol));
     }
   } else {
@@ -446,9 +505,23 @@ int tsqr_alloc(Ctx* h) {
     ts->nlev = 0;
   } else {
   // leaf block rows: user's choice or ~1024 (512 when s_max > 8)
-  int nb = h->cfg.block_rows > 0 ? h->cfg.block_rows : (wmax > 8 ? 512 : 1024);
+  const int RB = wmax > 8 ? 512 : 1024;  // rows a two-group level kernel holds per block
+  int nb = h->cfg.block_rows > 0 ? h->cfg.block_rows : RB;
   nb = std::max(nb, 2 * cap);
   if (nb < cap || n < cap) return PQR_EPLAN;
+  // FlatTSPQR chains (§4.2, Alg. 10; WyLevel): a chained block's carry rows live
+  // outside the register file but the tail's s pivot rows, which take the last wmax register rows
+  // (own rows <= RB - wmax); used when every chain gets several blocks (cfg.chains:
+  // PQR_CHAINS_AUTO, _OFF, _ON = whenever there are more leaf blocks than chains)
+  const int NC = 2 * h->sms;
+  const int own = h->cfg.block_rows > 0 ? nb : RB - wmax;
+  int cmode = h->cfg.chains;
+  if (const char* e = getenv("PQR_CHAINS"))  // A/B aid: overrides the handle's setting
+    cmode = !strcmp(e, "off") ? PQR_CHAINS_OFF : !strcmp(e, "on") ? PQR_CHAINS_ON : PQR_CHAINS_AUTO;
+  // (AUTO = the pure tree: on B200 the chained leaf kernels are measured slower than the tree
+  // levels they replace)
+  const bool chains = cmode == PQR_CHAINS_ON && own >= cap && own <= RB - wmax && n / own >= (int64_t)NC + 1;
+  if (chains) nb = own;
   int64_t p0 = std::max<int64_t>(1, (n + nb - 1) / nb);
   // the largest block (q, + 2 for the first rem2 blocks, + 1 odd row) must not exceed nb
   auto max_rows = [&](int64_t p) {
@@ -465,13 +538,18 @@ int tsqr_alloc(Ctx* h) {
   leaf.odd_last = (int)(rest & 1);
   leaf.rows = h->ld;
   leaf.ldv = h->ld;
+  leaf.chained = chains;
   ts->nb = nb;
+  ts->nchain = chains ? NC : 0;
   TRY(alloc_level(h, leaf, wmax, false));
+  if (chains) {
+    if ((rc = dalloc(&ts->VC, (size_t)p0 * cap * (wmax + 2)))) return rc;
+  }
   if (n & 1)  // zero pad row n of every reflector column (bulk copies of the odd last block read it)
     CUDA_TRY(cudaMemset2DAsync(leaf.V + n, leaf.ldv * sizeof(double), 0, sizeof(double), cap, h->stream));
   ts->lv.clear();
   ts->lv.push_back(leaf);
-  int pl = (int)p0;
+  int pl = chains ? NC : (int)p0;  // children of the first node level: chains or leaf blocks
   while (pl > 1) {
     pl = (pl + ts->arity - 1) / ts->arity;
     TsqrLv nd;
@@ -524,6 +602,7 @@ int tsqr_alloc(Ctx* h) {
   }
   h->st.block_rows = lpip(h) ? 0 : (int)ts->lv[0].q;
   h->st.tree_levels = ts->nlev;
+  h->st.leaf_chains = ts->nchain;
   return PQR_OK;
 }
 
@@ -574,11 +653,17 @@ int tsqr_create(Ctx* h, const double* Q, int64_t ldq, int k) {
 }
 
 // start rows of the leaf blocks (nblocks + 1 entries, the last = n_local): host-pipeline chunking
+// (chained leaves: one entry per round of nchain blocks; leaf_chunk maps units back to blocks)
 void tsqr_leaf_bounds(Ctx* h, std::vector<int64_t>* out) {
   const TsqrLv& lv = h->ts->lv[0];
-  out->resize((size_t)lv.nblocks + 1);
-  for (int64_t b = 0; b < lv.nblocks; ++b) (*out)[b] = b * lv.q + 2 * std::min<int64_t>(b, lv.rem2);
-  (*out)[lv.nblocks] = h->cfg.n_local;
+  const int64_t unit = h->ts->nchain > 0 ? h->ts->nchain : 1;
+  const int64_t nu = (lv.nblocks + unit - 1) / unit;
+  out->resize((size_t)nu + 1);
+  for (int64_t u = 0; u < nu; ++u) {
+    const int64_t b = u * unit;
+    (*out)[u] = b * lv.q + 2 * std::min<int64_t>(b, lv.rem2);
+  }
+  (*out)[nu] = h->cfg.n_local;
 }
 
 int tsqr_solve(Ctx* h, const double* X, int64_t ldx, int s, unsigned flags, double* Ud, int64_t ldud, bool append,
@@ -692,6 +777,7 @@ void tsqr_free(Ctx* h) {
   cudaFree(ts->Ut);
   cudaFree(ts->Rt);
   cudaFree(ts->coef);
+  cudaFree(ts->VC);
   cudaFree(ts->d_pan);
   cudaFree(ts->d_panm);
   delete ts;

@@ -43,15 +43,6 @@ namespace pqr {
 // 16 consumer warps per CTA, as one group or as two groups of 8 on alternate blocks (see the
 // kernels at the end); UW below is per-warp units for the group's warp count, the host plans
 // in 16-warp units.
-#ifndef PQR_WY_ONEBAR8
-#define PQR_WY_ONEBAR8 1
-#endif
-#ifndef PQR_WY_ONEBAR16
-#define PQR_WY_ONEBAR16 1
-#endif
-#ifndef PQR_WY_ROT16
-#define PQR_WY_ROT16 1  // 16-column tail: rotated register file (0: select-chain loop)
-#endif
 constexpr int kWyWarps = 16;                     // consumer warps per CTA
 constexpr int kWyThreads = 32 * kWyWarps;        // consumer threads
 constexpr int kWyLaunch = kWyThreads + 128;      // + one producer warpgroup (one working lane)
@@ -84,6 +75,24 @@ struct WyLevel {
   int wmax;                         // widest panel (<= 16) -> smem slot width
   int nbuf;                         // ring slots (>= 2)
   unsigned long long* trace;        // optional phase-cycle counters (tools; nullptr = off)
+  // FlatTSPQR chains (§4.2, Alg. 10, Eqs. flat_tsqr / flattspqr_q; leaf level only,
+  // nchain = 0 elsewhere): block b continues chain b % nchain.  A "chained" block (b >= nchain)
+  // solves the stacked problem [K; X_b], K = the chain's [P; N] so far ((C+s) x s, the previous
+  // block's output, kept in the chain slot out + (b % nchain) * cap), so each chain hands one block
+  // to the tree instead of one per leaf block.  The carry rows K are not held in the register
+  // file: reflector j of a chained block is non-zero on the carry rows only in its panel's rows
+  // [x, x + w) (below C+s the carry is zero, and a panel's reflectors start at its own pivot
+  // rows), so a panel touches only K[x : x+w, :] — read once and written once, by warp 0:
+  //   Z += K[x:x+w]^T Vc (one more MMA pair in warp 0's partial),  K[x:x+w] -= Vc Z'  (-> slot),
+  // and the stage-1 tail's pivot rows C+c are the carry rows [C, C+s) (warp 0, in shared memory),
+  // every own row lying below every pivot.  Stage 2 walks a chain backwards: K = the block's
+  // coefficients (cin slot), own rows start at zero, and the updated K is the coefficient block of
+  // the chain's previous block (written back into the cin slot).  Launches of a chained level use
+  // grid = nchain / NG and b0 a multiple of nchain.
+  // Storage of the carry part of reflector j: rows [j & ~1, (j & ~1) + LS), LS = wmax + 2, at
+  // VC + (b*cap + j)*LS; a panel's columns are contiguous there (one bulk copy per panel).
+  int nchain, LS;
+  double* VC;
 };
 
 struct WyPanels {
@@ -97,14 +106,17 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
 }
 
 // per-group scratch (doubles) of a level kernel with NW consumer warps per group:
-// partials (NW + 1) E, Z (E), Householder-round buffers, diag, T scratch, round coefficients
+// partials (NW + 1) E, Z (E), Householder-round buffers, diag, T scratch, round coefficients,
+// a chained block's carry rows: the stage-1 tail's (E) and two panels' (2 E)
 PQR_HOST_DEV constexpr int wy_group_scratch(int NW, int E) {
-  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 64 + 16 * NW;
+  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 64 + 3 * E;
 }
+// ring slot (doubles): a panel (RP x wm), its T (wm x wm), its columns' carry segments (wm x LS)
+PQR_HOST_DEV constexpr int wy_slot(int RP, int wm) { return RP * wm + wm * wm + wm * (wm + 2); }
 // shared-memory bytes of a level kernel (host and device agree on this layout)
 inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf, int NW, int NG) {
   const int E = wmax * wmax;
-  return ((size_t)nbuf * (RP * wmax + 256) + (size_t)NG * wy_group_scratch(NW, E)) * sizeof(double) +
+  return ((size_t)nbuf * wy_slot(RP, wmax) + (size_t)NG * wy_group_scratch(NW, E)) * sizeof(double) +
          (size_t)(cap + 2) * sizeof(int4) + (size_t)2 * nbuf * sizeof(uint64_t) + 16;
 }
 
@@ -112,7 +124,7 @@ inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf, int NW, int NG)
 // CTA's blocks alternately (group g: its blocks jb = g, g + 2, ...), each with its own scratch
 // and named barrier; the producer streams the items in block order as for one group, so while
 // one group runs its block's Householder tail the other applies its panels.
-template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false, int NG = 1>
+template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false, int NG = 1, bool CH = false>
 PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge_,
                      int mtoff) {
   constexpr int NTH = 32 * NW, NLA = NTH * NG + 128;  // consumer threads per group, launch size
@@ -123,7 +135,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   extern __shared__ __align__(16) double sm[];
   constexpr int wm = WM, MTM = WM / 8;  // widest panel (8 or 16) and its 8-column tiles
   const int RP = L.RP, nbuf = L.nbuf;
-  const int SS = RP * wm + 256;  // slot: panel (RP x wm) + its T
+  const int SS = wy_slot(RP, wm);  // slot: panel (RP x wm), its T, its carry segments
   const int E = wm * wm;
   const int gtid = threadIdx.x, gwarp = gtid >> 5;
   const int grp = NG > 1 ? (gwarp < NW ? 0 : 1) : 0;  // (producer warps: irrelevant)
@@ -135,7 +147,11 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   double* diagv = hred + 2 * (NW * kWyHS + 16);  // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
   double* hfc = tsc + 512;                 // 2 x 32: Householder-round coefficients (by round parity)
-  double* hupd = hfc + 64;                 // NW x 16: per-warp round coefficients (16-column tail)
+  double* ctl = hfc + 64;                  // E: carry rows [C, C+s) of a chained block's tail (row-major, ld 8*NT)
+  double* kbuf = ctl + E;                  // 2 x E: K[x : x+w, :] of a chained block's panels (ld wm), by panel parity
+  // NW x 16 per-warp round coefficients of the 16-column tail: the T-column half of tsc, which the
+  // rounds leave free (T is formed after them)
+  double* hupd = tsc + 256;
   int4* pans = reinterpret_cast<int4*>(ring + (size_t)nbuf * SS + NG * GS);
   uint64_t* full = reinterpret_cast<uint64_t*>(pans + L.cap + 2);
   uint64_t* empty = full + nbuf;
@@ -151,6 +167,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   const int64_t nbl = L.nrun;
   const int nb_cta = (int64_t)blockIdx.x < nbl ? (int)((nbl - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int64_t total = (int64_t)nb_cta * ipb;
+  const bool chains = CH && L.nchain > 0;  // (CH: separate instantiations; others carry no chain code)
+  constexpr int LS = WM + 2;              // carry segment rows (WyLevel::LS)
+  const bool rev = chains && !UP;  // stage 2 walks the chains backwards
 
   // never-copied slot parts must hold finite values (they meet zero coefficients)
   for (int e = gtid; e < nbuf * SS; e += NLA) ring[e] = 0.0;
@@ -172,8 +191,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     if constexpr (NW * NG == 16) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kWyProducerRegs));
     if (gwarp == NW * NG && lane == 0) {
       for (int it = 0; it < total; ++it) {
-        const int jb = it / ipb;
-        const int p = it - jb * ipb;
+        const int pos = it / ipb;
+        const int jb = rev ? nb_cta - 1 - pos : pos;
+        const int p = it - pos * ipb;
         const int slot = it % nbuf;
         // (sleeping between polls: the power-capped bench runs ~0.7 % faster)
         if (it >= nbuf) mbar_wait_sleep(&empty[slot], (uint32_t)((it / nbuf - 1) & 1));
@@ -192,10 +212,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           const int4 pn = pans[UP ? p - 1 : np - 1 - p];
           const int Rc = R + (R & 1);  // includes the zero pad row of an odd block
           const uint32_t tb = (uint32_t)((pn.y * pn.y + 1) & ~1) * 8u;
-          mbar_arrive_expect_tx(bar, (uint32_t)pn.y * Rc * 8u + tb);
+          const bool chained = chains && b >= L.nchain;
+          const uint32_t cb = chained ? (uint32_t)(pn.y * LS) * 8u : 0u;  // the columns' carry segments
+          mbar_arrive_expect_tx(bar, (uint32_t)pn.y * Rc * 8u + tb + cb);
           for (int j = 0; j < pn.y; ++j)
             bulk_g2s(buf + j * RP, L.V + (int64_t)(pn.x + j) * L.ldv + r0, (uint32_t)Rc * 8u, bar);
           bulk_g2s(buf + RP * wm, L.T + b * L.tstride + pn.z, tb, bar);
+          if (chained) bulk_g2s(buf + RP * wm + wm * wm, L.VC + (b * L.cap + pn.x) * LS, cb, bar);
         }
         if constexpr (NG > 1) {
           __threadfence_block();
@@ -262,12 +285,55 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 
   int64_t it = 0;  // consumer item cursor
   int hpar = 0;    // Householder-round buffer parity
-  for (int jb = grp; jb < nb_cta; jb += NG) {
-    it = (int64_t)jb * ipb;  // this block's first ring item
+  const int ncnt = nb_cta > grp ? (nb_cta - grp + NG - 1) / NG : 0;  // this group's blocks
+  for (int kb = 0; kb < ncnt; ++kb) {
+    const int jb = rev ? grp + (ncnt - 1 - kb) * NG : grp + kb * NG;
+    it = (int64_t)(rev ? nb_cta - 1 - jb : jb) * ipb;  // this block's first ring item
     const int64_t b = L.b0 + blockIdx.x + (int64_t)jb * gridDim.x;
     const int64_t r0 = wy_start(L, b);
     const int R = wy_rows(L, b);
-    const bool mrow = 16 * UW * (warp + 1) > R;  // warp holds rows >= R
+    const bool chained = chains && b >= L.nchain;  // stacked problem [K; X_b] (see WyLevel)
+    const int Rt = R;
+    const int64_t cslot = chains ? b % L.nchain : b;  // output (stage 1) / coefficient (stage 2) slot
+    // K: the chain slot (stage 1: the chain's [P; N], updated in place into this block's output;
+    // stage 2: the coefficients, updated in place into the previous block's)
+    double* kslot = UP ? L.out + cslot * L.cap : const_cast<double*>(L.cin) + cslot * L.cap;
+    const int64_t kld = UP ? L.ldo : L.ldci;
+    // the chain slot is re-read one block later (by the chain's next block) while tens of MB stream
+    // through L2: it is written and read with an evict-last policy so that it stays resident
+    const uint64_t kpol = chains ? l2_evict_last() : 0ull;
+    const bool mrow = 16 * UW * (warp + 1) > Rt;  // warp holds rows >= Rt
+    // The chain's previous block (this group's previous one) wrote the slot read below: across
+    // warps when either block is a chain's first (its rows are in every warp), else warp 0 to
+    // warp 0.
+    if (chains && kb > 0) {
+      const bool xw = UP ? (chained && b - L.nchain < L.nchain) : !chained;
+      if (xw) cbar();
+      else __syncwarp();
+    }
+    // chained block, warp 0: K rows of panel p into kbuf[p & 1] by cp.async, one commit group per
+    // panel (panel p + 1's rows are fetched while panel p runs; a panel's rows are disjoint from
+    // every other panel's, so the prefetch never reads a row an earlier panel rewrites)
+    auto kfetch = [&](int pp) {
+      if (pp < np) {
+        const int4 pn = pans[UP ? pp : np - 1 - pp];
+        double* dst = kbuf + (pp & 1) * E;
+        for (int e = lane; e < wm * s; e += 32) {
+          const int i = e % wm, c = e / wm;  // (rows i >= w are never read)
+          if (i < pn.y) cp_async8_l2pol(dst + i + wm * c, kslot + pn.x + i + (int64_t)c * kld, kpol);
+        }
+      }
+      cp_async_commit();
+    };
+    if (chained && UP && warp == NW - 1) {  // the stage-1 tail's carry rows [C, C+s) (no panel touches them)
+      for (int e = lane; e < 8 * NT * 8 * NT; e += 32) {
+        const int i = e / (8 * NT), col = e % (8 * NT);
+        if (i < s && col < s) cp_async8_l2pol(ctl + e, kslot + C + i + (int64_t)col * kld, kpol);
+        else ctl[e] = 0.0;
+      }
+      cp_async_commit();
+    }
+    if (chained && warp == 0) kfetch(0);
     double x[UW][NT][4];
     if (UP) {
       WY_TR(9);
@@ -285,14 +351,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int i = 0; i < 4; ++i) {
             const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
             double v = 0.0;
-            if (c < s && row < R)
-              v = (row == R - 1 && (R & 1)) ? L.X[r0 + row + (int64_t)c * L.ldx] : buf[c * RP + row];
+            if (c < s && row < Rt) v = (row == Rt - 1 && (R & 1)) ? L.X[r0 + row + (int64_t)c * L.ldx] : buf[c * RP + row];
             x[u][nt][i] = v;
           }
       release(it);
       ++it;
     } else {
-      const double* cb = L.cin + b * L.cap;
+      const double* cb = L.cin + cslot * L.cap;
 #pragma unroll
       for (int u = 0; u < UW; ++u)
 #pragma unroll
@@ -300,7 +365,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
-            x[u][nt][i] = (row < Call && row < R && c < s) ? cb[row + (int64_t)c * L.ldci] : 0.0;
+            // (a chained block's coefficients are all carry rows: its own rows start at zero)
+            x[u][nt][i] = (!chained && row < Call && row < Rt && c < s) ? cb[row + (int64_t)c * L.ldci] : 0.0;
           }
     }
 
@@ -317,6 +383,48 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       const int w = pans[UP ? p : np - 1 - p].y;
       const int mtn = (w + 7) >> 3;
       double zp[NT][MTM][2];
+      // chained block: warp 0 also carries the panel's carry rows K[px : px+w] (see WyLevel)
+      const int px = pans[UP ? p : np - 1 - p].x;
+      const bool kw = chained && warp == 0;
+      const double* vcs = Tg + wm * wm;  // the panel's carry segments: column j at j*LS
+      // carry part of reflector px + j on stacked row r (zero outside [px + j, px + w))
+      auto vcar = [&](int r, int j) -> double {
+        return (j < w && r >= px + j && r < px + w) ? vcs[j * LS + r - ((px + j) & ~1)] : 0.0;
+      };
+      const double* kb = kbuf + (p & 1) * E;  // K[px + i][c] at kb[i + wm c]
+      if (kw) kfetch(p + 1);
+      // this panel's K rows have landed (waited for right before their first use)
+      auto kready = [&]() {
+        cp_async_wait<1>();
+        __syncwarp();
+      };
+      // K[px + 4kk + q][8nt + g] (zero outside the panel's rows and the block's columns)
+      auto kcar = [&](int nt, int kk) -> double {
+        const int i = 4 * kk + q, c = 8 * nt + g;
+        return (i < w && c < s) ? kb[i + wm * c] : 0.0;
+      };
+      // K[px : px+w] -= Vc Z' (Z'(j, c) from shared memory), written back to the slot: per 8 x 8
+      // tile D[c][i] = sum_j Z'(j, c) Vc(px + i, j) by MMAs (A = Z'^T, B = Vc^T)
+      auto carry_update = [&](const double* zsrc, int zld) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int ti = 0; ti < MTM; ++ti) {
+            const int c = 8 * nt + g;
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 2 * MTM; ++kk) {
+              const int j = 4 * kk + q;
+              const double a = (j < w && c < s) ? zsrc[j + zld * c] : 0.0;
+              dmma884(d0, d1, a, vcar(px + 8 * ti + g, j));
+            }
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int i = 8 * ti + 2 * q + v;  // D[c][i] in (d0, d1)
+              if (i < w && c < s) st_l2pol(kslot + px + i + (int64_t)c * kld, kb[i + wm * c] - (v ? d1 : d0), kpol);
+            }
+          }
+      };
       if constexpr (MTM == 1) {
         // 8-wide panels (stage 1 too since the two-group kernels: 6.65 -> 6.37 ms; with one
         // 16-warp group it was slower there): each warp forms its partial of Z^T = x^T V (A = x from registers,
@@ -342,6 +450,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             dmma884(ac[0], ac[1], x[u][nt][2], a23.x);
             dmma884(ac[0], ac[1], x[u][nt][3], a23.y);
           }
+        }
+        if (kw) {  // + K[px:px+w]^T Vc (rows px + 4kk + q)
+          kready();
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) dmma884(acc[kk][nt][0], acc[kk][nt][1], kcar(nt, kk), vcar(px + 4 * kk + q, g));
         }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -375,6 +490,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           zp[nt][0][0] = z2.x;
           zp[nt][0][1] = z2.y;
         }
+        if (kw) carry_update(Zs, wm);  // Zs[j + wm c] = Z'(j, c)
       } else {
       // Z = V^T x: per-warp partials, two accumulator chains over alternate units
       double acc[2][MTM][NT][2];
@@ -402,6 +518,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
               dmma884(ac[0], ac[1], a23.y, x[u][nt][3]);
             }
           }
+          if (kw) {  // + Vc^T K[px:px+w] (rows px + 4kk + q)
+            if (mt == 0) kready();
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                dmma884(acc[kk & 1][mt][nt][0], acc[kk & 1][mt][nt][1], vcar(px + 4 * kk + q, 8 * mt + g), kcar(nt, kk));
+          }
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -421,7 +545,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       // 8-wide panels: every warp forms it (two MMAs).  16-wide panels: warps 0-3 form one
       // 8x8 tile each into shared memory (tsc: free outside the stage-1 tail) behind one
       // more barrier, instead of 16 MMAs in every warp.
-      const bool shared_zp = NT > 1 && mtn == 2;
+      // (a chained block always: warp 0's carry update reads Z' from tsc)
+      const bool shared_zp = (NT > 1 && mtn == 2) || chained;
       if (MTM == 2 && shared_zp) {
         if (warp < 4) {
           const int jt = warp >> 1, nt = warp & 1, jj = 8 * jt + g;
@@ -429,7 +554,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int l = 4 * k4 + q;
-            const double a = Zs[l + wm * (8 * nt + g)];
+            const double a = l < 8 * mtn ? Zs[l + wm * (8 * nt + g)] : 0.0;
             const double bt = (l < w && jj < w) ? (UP ? Tg[l + w * jj] : Tg[jj + w * l]) : 0.0;
             dmma884(d0, d1, a, bt);
           }
@@ -438,6 +563,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           tsc[(8 * jt + 2 * q + 1) + 16 * (8 * nt + g)] = d1;
         }
         cbar();
+        if (kw) carry_update(tsc, 16);  // tsc[j + 16 c] = Z'(j, c)
       }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -481,7 +607,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           }
         }
       }
-      if (!(UP && merge && p == np - 1)) release(it);  // merging: the last panel stays for the tail
+      if (!(UP && merge && p == np - 1)) {  // merging: the last panel stays for the tail
+        release(it);
+      }
       WY_TR(6);
       if (mrow) {  // rows >= R stay zero (stale slot rows may be non-zero)
 #pragma unroll
@@ -490,12 +618,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (16 * (warp * UW + u) + 4 * q + i >= R) x[u][nt][i] = 0.0;
+              if (16 * (warp * UW + u) + 4 * q + i >= Rt) x[u][nt][i] = 0.0;
       }
     }
 
     if constexpr (!UP) {
       // ---------------- stage-2 output: Y_b (columns >= t written as zero) ----------------
+      // (a chained block's carry coefficients went back into the chain slot panel by panel)
 #pragma unroll
       for (int u = 0; u < UW; ++u)
 #pragma unroll
@@ -508,11 +637,11 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
           for (int i = 0; i < 4; i += 2) {
             const double v0 = ok ? x[u][nt][i] : 0.0, v1 = ok ? x[u][nt][i + 1] : 0.0;
-            if (L.yvec && row + i + 1 < R) {
+            if (L.yvec && row + i + 1 < Rt) {
               st2(yp + i, v0, v1);
             } else {
-              if (row + i < R) yp[i] = v0;
-              if (row + i + 1 < R) yp[i + 1] = v1;
+              if (row + i < Rt) yp[i] = v0;
+              if (row + i + 1 < Rt) yp[i + 1] = v1;
             }
           }
         }
@@ -528,8 +657,26 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     //   v_c' . v_c by the same formula for c' < c (column c of V^T V, for T).
     constexpr int RPL = UW / 2;   // rows per lane in the row layout
     constexpr int S8 = 8 * NT;    // columns per row
-    // one barrier per Householder round (every warp forms the scalars) or two (warp 0 forms them)
-    constexpr bool ONEBAR = S8 == 8 ? PQR_WY_ONEBAR8 : PQR_WY_ONEBAR16;
+    // Chained block: the tail's pivot rows C + c are the carry rows [C, C+s) (the chain's N so far;
+    // no panel touches them).  They take the spare register rows [crow, crow + s) at the end of the
+    // group's rows (chained blocks hold <= crow own rows) and join the rounds like own rows, with
+    // stacked index C + (row - crow); every own row lies below every pivot.
+    constexpr int crow = 16 * NW * UW - WM;
+    if (chained) {
+      if (warp == NW - 1) {  // ctl was fetched by this warp at the block's start
+        cp_async_wait<0>();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int u = 0; u < UW; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = 16 * (warp * UW + u) + 4 * q + i, c = 8 * nt + g;
+            if (row >= crow) x[u][nt][i] = (row - crow < s && c < s) ? ctl[(row - crow) * S8 + c] : 0.0;
+          }
+    }
     double xr[RPL][S8];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -565,6 +712,12 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       const int sg = g * RPL + e;
       rowk[e] = 16 * (warp * UW + (sg >> 2)) + 4 * q + (sg & 3);
     }
+    // stacked row index of each of this lane's rows (chained: own rows below every pivot, carry rows
+    // at C + (row - crow), unused rows never >= a pivot)
+    int srow[RPL];
+#pragma unroll
+    for (int e = 0; e < RPL; ++e)
+      srow[e] = !chained ? rowk[e] : (rowk[e] < R ? (1 << 24) : (rowk[e] >= crow && rowk[e] - crow < s ? C + rowk[e] - crow : -1));
     double* Gs = tsc;  // strict upper part of V^T V (ld 16), column c written in round c by tid 0
     // Round scalars, formed by every warp from the NW warp partials of hb (the same fixed summation
     // order in every warp and lane: bitwise-identical values), so a round needs one barrier:
@@ -597,43 +750,6 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         if (lane == 0) diagv[c] = diag;
       }
     };
-    // Two-barrier form: warp 0 alone forms the scalars and publishes them (hfc, by round parity)
-    // behind a second barrier.
-    auto round_scalars_w0 = [&](int c, const double* hb, double (&fvc)[S8], double& inv, double& wr) {
-      double* hf = hfc + (c & 1) * 32;  // [0, S8): coefficients; S8: inv; S8+1: u0 - sigma*lambda
-      if (warp == 0) {
-        constexpr int NP = 32 / S8, WPP = NW / NP;
-        const int v = lane & (S8 - 1), part = lane / S8;
-        const double* hv = hb + part * WPP * kWyHS + v;
-        double tot = 0.0;
-#pragma unroll
-        for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
-#pragma unroll
-        for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
-        const double lam2 = __shfl_sync(0xffffffffu, tot, c);
-        const double u0 = hb[NW * kWyHS + c];
-        const double lam = sqrt(lam2);
-        const double sigma = (u0 >= 0.0) ? -1.0 : 1.0;
-        const double diag = sigma * lam;
-        const double nv2 = 2.0 * lam * (lam + fabs(u0));
-        const double iv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;
-        const double fv = v == c ? 0.0 : 2.0 * iv * (tot - diag * hb[NW * kWyHS + v]);
-        if (lane < S8) {
-          hf[lane] = fv;
-          if (lane < c) Gs[lane + 16 * c] = 0.5 * fv;
-        }
-        if (lane == 0) {
-          hf[S8] = iv;
-          hf[S8 + 1] = u0 - diag;
-          diagv[c] = diag;
-        }
-      }
-      cbar();
-      inv = hf[S8];
-      wr = hf[S8 + 1];
-#pragma unroll
-      for (int cc = 0; cc < S8; ++cc) fvc[cc] = hf[cc];
-    };
     WY_TR(10);
     if constexpr (S8 == 8) {
 #pragma unroll
@@ -645,7 +761,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       for (int cc = 0; cc < S8; ++cc) D[cc] = 0.0;
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
-        if (rowk[e] >= r) {
+        if (srow[e] >= r) {
 #pragma unroll
           for (int cc = 0; cc < S8; ++cc) D[cc] = fma(xr[e][c], xr[e][cc], D[cc]);
         }
@@ -669,7 +785,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       if ((lane & (LG - 1)) == 0) hb[warp * kWyHS + vi] = D[0];
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
-        if (rowk[e] == r) {
+        if (srow[e] == r) {
 #pragma unroll
           for (int cc = 0; cc < S8; ++cc) hb[NW * kWyHS + cc] = xr[e][cc];
         }
@@ -678,23 +794,19 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       WY_TR(12);
       double fvc[S8];
       double inv, wr;
-      if constexpr (ONEBAR) {
-        round_scalars(c, hb, fvc, inv, wr);
-      } else {
-        round_scalars_w0(c, hb, fvc, inv, wr);
-      }
+      round_scalars(c, hb, fvc, inv, wr);
       WY_TR(13);
 #pragma unroll
       for (int e = 0; e < RPL; ++e)
-        if (rowk[e] >= r) {
-          const double vv = (rowk[e] == r ? wr : xr[e][c]) * inv;
+        if (srow[e] >= r) {
+          const double vv = (srow[e] == r ? wr : xr[e][c]) * inv;
 #pragma unroll
           for (int cc = c + 1; cc < S8; ++cc) xr[e][cc] = fma(-fvc[cc], vv, xr[e][cc]);
           xr[e][c] = vv;
         }
     }
     } else {
-    if constexpr (PQR_WY_ROT16) {
+    {
     // 16 columns, rotated register file: entering a group of RU rounds with base c0, xr[e][j] holds
     // column (c0 + j) mod 16, so round c = c0 + cj pivots on the compile-time index cj and every
     // register index is static (no select chains, no per-column predicates); the group ends by
@@ -714,7 +826,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           for (int j = 0; j < S8; ++j) D[j] = 0.0;
 #pragma unroll
           for (int e = 0; e < RPL; ++e)
-            if (rowk[e] >= r) {
+            if (srow[e] >= r) {
 #pragma unroll
               for (int j = 0; j < S8; ++j) D[j] = fma(xr[e][cj], xr[e][j], D[j]);
             }
@@ -735,7 +847,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           if ((lane & 1) == 0) hb[warp * kWyHS + vi] = D[0];
 #pragma unroll
           for (int e = 0; e < RPL; ++e)
-            if (rowk[e] == r) {
+            if (srow[e] == r) {
 #pragma unroll
               for (int j = 0; j < S8; ++j) hb[NW * kWyHS + j] = xr[e][j];
             }
@@ -780,8 +892,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           }
 #pragma unroll
           for (int e = 0; e < RPL; ++e)
-            if (rowk[e] >= r) {
-              const double vv = (rowk[e] == r ? wr : xr[e][cj]) * inv;
+            if (srow[e] >= r) {
+              const double vv = (srow[e] == r ? wr : xr[e][cj]) * inv;
 #pragma unroll
               for (int j = 0; j < S8; ++j)
                 if (j != cj) xr[e][j] = fma(-up[j], vv, xr[e][j]);
@@ -799,75 +911,6 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
         for (int j = 0; j < S8; ++j) xr[e][j] = tmp[j];
       }
-    }
-    } else {
-    // 16 columns: the rounds stay a loop (fully unrolled they overflow the instruction cache);
-    // column c of a row is picked with a select chain instead of a dynamic register index
-#pragma unroll 1
-    for (int c = 0; c < S8; ++c) {
-      if (c >= s) break;
-      const int r = C + c;
-      double xc[RPL];
-#pragma unroll
-      for (int e = 0; e < RPL; ++e) {
-        double v = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < S8; ++cc) v = cc == c ? xr[e][cc] : v;
-        xc[e] = v;
-      }
-      double D[S8];
-#pragma unroll
-      for (int cc = 0; cc < S8; ++cc) D[cc] = 0.0;
-#pragma unroll
-      for (int e = 0; e < RPL; ++e)
-        if (rowk[e] >= r) {
-#pragma unroll
-          for (int cc = 0; cc < S8; ++cc) D[cc] = fma(xc[e], xr[e][cc], D[cc]);
-        }
-#pragma unroll
-      for (int mb = 16, w = S8; w > 1; mb >>= 1, w >>= 1) {
-        const bool up = (lane & mb) != 0;
-#pragma unroll
-        for (int j = 0; j < w / 2; ++j) {
-          const double send = up ? D[j] : D[j + w / 2];
-          const double keep = up ? D[j + w / 2] : D[j];
-          D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
-        }
-      }
-      constexpr int LG = S8 == 8 ? 4 : 2;
-      D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
-      if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
-      const int vi = (lane / LG) & (S8 - 1);
-      double* hb = hred + hpar * (NW * kWyHS + 16);
-      hpar ^= 1;
-      if ((lane & (LG - 1)) == 0) hb[warp * kWyHS + vi] = D[0];
-#pragma unroll
-      for (int e = 0; e < RPL; ++e)
-        if (rowk[e] == r) {
-#pragma unroll
-          for (int cc = 0; cc < S8; ++cc) hb[NW * kWyHS + cc] = xr[e][cc];
-        }
-      WY_TR(11);
-      cbar();  // the round's only barrier
-      WY_TR(12);
-      double fvc[S8];
-      double inv, wr;
-      if constexpr (ONEBAR) {
-        round_scalars(c, hb, fvc, inv, wr);
-      } else {
-        round_scalars_w0(c, hb, fvc, inv, wr);
-      }
-      WY_TR(13);
-#pragma unroll
-      for (int e = 0; e < RPL; ++e)
-        if (rowk[e] >= r) {
-          const double vv = (rowk[e] == r ? wr : xc[e]) * inv;
-#pragma unroll
-          for (int cc = 0; cc < S8; ++cc) {
-            if (cc > c) xr[e][cc] = fma(-fvc[cc], vv, xr[e][cc]);
-            else if (cc == c) xr[e][cc] = vv;
-          }
-        }
     }
     }
     }
@@ -909,7 +952,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           const double a1 = v1[j * RP + row];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const double v2 = row >= C + c ? xr[e][c] : 0.0;
+            const double v2 = srow[e] >= C + c ? xr[e][c] : 0.0;
             Dp[j * 4 + c] = fma(a1, v2, Dp[j * 4 + c]);
           }
         }
@@ -967,8 +1010,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     // With RPL even a lane's rows come in consecutive pairs (rowk[e + 1] = rowk[e] + 1 for even e),
     // so a warp writes each column as one contiguous 16-byte-per-lane store.
     {
-      double* outb = L.out + b * L.cap;
-      const int rmax = R < L.orows ? R : L.orows;
+      double* outb = L.out + cslot * L.cap;
+      // (a chained block's outputs are its carry rows, below; its own rows hold only reflectors)
+      const int rmax = chained ? 0 : (Rt < L.orows ? Rt : L.orows);
 #pragma unroll
       for (int c = 0; c < S8; ++c) {
         if (c >= s) break;
@@ -978,16 +1022,17 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         double* ocol = outb + (int64_t)c * L.ldo;
 #pragma unroll
         for (int e = 0; e < RPL; ++e) {
-          const int row = rowk[e];
-          const double ov = row < piv ? xr[e][c] : (row == piv ? dg : 0.0);
-          const double vv = row >= piv ? xr[e][c] : 0.0;
+          const int row = rowk[e], sr = srow[e];
+          const double ov = sr < piv ? xr[e][c] : (sr == piv ? dg : 0.0);
+          const double vv = sr >= piv ? xr[e][c] : 0.0;
           if constexpr (RPL % 2 == 0) {
             if (e % 2 == 0) {
-              const double ov1 = row + 1 < piv ? xr[e + 1][c] : (row + 1 == piv ? dg : 0.0);
-              const double vv1 = row + 1 >= piv ? xr[e + 1][c] : 0.0;
-              if (row + 1 < R) {
+              const int sr1 = srow[e + 1];
+              const double ov1 = sr1 < piv ? xr[e + 1][c] : (sr1 == piv ? dg : 0.0);
+              const double vv1 = sr1 >= piv ? xr[e + 1][c] : 0.0;
+              if (row + 1 < Rt) {
                 st2(vcol + row, vv, vv1);
-              } else if (row < R) {
+              } else if (row < Rt) {
                 vcol[row] = vv;
               }
               if (L.ovec && row + 1 < rmax) {
@@ -999,9 +1044,33 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             }
           } else {
             if (row < rmax) ocol[row] = ov;
-            if (row < R) vcol[row] = vv;
+            if (row < Rt) vcol[row] = vv;
           }
         }
+      }
+      if (chained) {
+        // chained block: rows [C, C+s) of its output (the N part; rows < C were written panel by
+        // panel) from the carry register rows, and the carry parts of the new reflectors (rows
+        // [C + c, C + s) of column C + c) into their segments [xs, xs + LS), xs = (C + c) & ~1;
+        // warp 0 writes the segments' zero entries
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) {
+          const int sr = srow[e];
+          if (sr >= C && sr < C + s) {
+#pragma unroll
+            for (int c = 0; c < S8; ++c) {
+              if (c >= s) break;
+              st_l2pol(kslot + sr + (int64_t)c * kld, sr < C + c ? xr[e][c] : (sr == C + c ? diagv[c] : 0.0), kpol);
+              const int xs = (C + c) & ~1;
+              if (sr >= C + c) L.VC[(b * L.cap + C + c) * LS + sr - xs] = xr[e][c];
+            }
+          }
+        }
+        if (warp == 0)
+          for (int e = lane; e < s * LS; e += 32) {
+            const int c = e / LS, rr = ((C + c) & ~1) + e % LS;
+            if (!(rr >= C + c && rr < C + s)) L.VC[(b * L.cap + C + c) * LS + e % LS] = 0.0;
+          }
       }
     }
     }  // stage-1 tail
@@ -1017,15 +1086,15 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 // Level kernels: NG groups of 16 / NG consumer warps (UW in 16-warp units, as planned by the
 // host).  NG = 2 when a CTA gets two or more blocks (one group's tail overlaps the other's
 // panels), NG = 1 (16 warps on one block: lower latency per block) for the small tree levels.
-template <int UW, int NT, int WM, bool MERGE, int NG>
+template <int UW, int NT, int WM, bool MERGE, int NG, bool CH = false>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<kWyWarps / NG, UW * NG, NT, WM, true, MERGE, NG>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<kWyWarps / NG, UW * NG, NT, WM, true, MERGE, NG, CH>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
-template <int UW, int NT, int WM, int NG>
+template <int UW, int NT, int WM, int NG, bool CH = false>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_down(WyLevel L, WyPanels P, int Call, int t, int ncol) {
-  wy_body<kWyWarps / NG, UW * NG, NT, WM, false, false, NG>(L, P, 0, t, Call, ncol, 0, 0);
+  wy_body<kWyWarps / NG, UW * NG, NT, WM, false, false, NG, CH>(L, P, 0, t, Call, ncol, 0, 0);
 }
 
 }  // namespace pqr

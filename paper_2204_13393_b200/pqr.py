@@ -27,6 +27,8 @@ PQR_LOCAL_HH, PQR_LOCAL_PIP2 = 0, 1
 LOCALS = {"hh": PQR_LOCAL_HH, "pip2": PQR_LOCAL_PIP2}
 PQR_EXCHANGE_AUTO, PQR_EXCHANGE_COLLECTIVE, PQR_EXCHANGE_LSA = 0, 1, 2
 EXCHANGES = {"auto": PQR_EXCHANGE_AUTO, "collective": PQR_EXCHANGE_COLLECTIVE, "lsa": PQR_EXCHANGE_LSA}
+PQR_CHAINS_AUTO, PQR_CHAINS_OFF, PQR_CHAINS_ON = 0, 1, 2
+CHAINS = {"auto": PQR_CHAINS_AUTO, "off": PQR_CHAINS_OFF, "on": PQR_CHAINS_ON}
 
 
 class PQRError(RuntimeError):
@@ -42,6 +44,7 @@ class pqr_config(ctypes.Structure):
         ("block_rows", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
         ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("vgroup", ctypes.c_void_p),
         ("reduction", ctypes.c_int), ("local", ctypes.c_int), ("exchange", ctypes.c_int),
+        ("chains", ctypes.c_int),
     ]
 
 
@@ -50,7 +53,7 @@ class pqr_stats(ctypes.Structure):
         ("k", ctypes.c_int), ("last_t", ctypes.c_int), ("calls", ctypes.c_int64),
         ("collectives", ctypes.c_int64), ("collective_bytes", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64), ("block_rows", ctypes.c_int), ("tree_levels", ctypes.c_int),
-        ("exchange", ctypes.c_int),
+        ("exchange", ctypes.c_int), ("leaf_chains", ctypes.c_int),
     ]
 
 
@@ -164,7 +167,7 @@ def _stream_ptr(stream):
 # ---------------------------------------------------------------------------
 def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0.0, gram_eta=0.0, block_rows=0,
                stream=None, rank=0, nranks=1, nccl_id: bytes | None = None, vgroup=None, reduction="hh",
-               local="hh", exchange="auto"):
+               local="hh", exchange="auto", chains="auto"):
     cfg = pqr_config()
     cfg.n_local = int(n_local)
     cfg.k_max = int(k_max)
@@ -180,6 +183,7 @@ def pqr_create(n_local, k_max, s_max, Q=None, k=0, variant="cholqr2", defl_tol=0
     cfg.reduction = REDUCTIONS[reduction] if isinstance(reduction, str) else int(reduction)
     cfg.local = LOCALS[local] if isinstance(local, str) else int(local)
     cfg.exchange = EXCHANGES[exchange] if isinstance(exchange, str) else int(exchange)
+    cfg.chains = CHAINS[chains] if isinstance(chains, str) else int(chains)
     idbuf = None
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
