@@ -43,6 +43,9 @@ namespace pqr {
 // 16 consumer warps per CTA, as one group or as two groups of 8 on alternate blocks (see the
 // kernels at the end); UW below is per-warp units for the group's warp count, the host plans
 // in 16-warp units.
+#ifndef PQR_WY_ROT8
+#define PQR_WY_ROT8 0  // 8-column tail: 0 = fully unrolled rounds, RU > 0 = rotated, RU rounds per group
+#endif
 constexpr int kWyWarps = 16;                     // consumer warps per CTA
 constexpr int kWyThreads = 32 * kWyWarps;        // consumer threads
 constexpr int kWyLaunch = kWyThreads + 128;      // + one producer warpgroup (one working lane)
@@ -751,7 +754,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       }
     };
     WY_TR(10);
-    if constexpr (S8 == 8) {
+    if constexpr (S8 == 8 && PQR_WY_ROT8 == 0) {
 #pragma unroll
     for (int c = 0; c < S8; ++c) {
       if (c >= s) break;
@@ -812,7 +815,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     // register index is static (no select chains, no per-column predicates); the group ends by
     // rotating the columns by RU (16 rounds: back to identity).  Coefficients of finished columns
     // are zero, so the update is one unpredicated FMA per element (an exact no-op there).
-    constexpr int RU = 4;
+    // (8 columns too unless PQR_WY_ROT8 = 0: the fully unrolled 8 rounds make the kernel large
+    // enough to miss in the instruction cache while the other group runs the panel code)
+    constexpr int RU = S8 == 8 ? (PQR_WY_ROT8 > 0 ? PQR_WY_ROT8 : 1) : 4;
     double* wup = hupd + warp * 16;  // this warp's update coefficients of the round
 #pragma unroll 1
     for (int c0 = 0; c0 < S8; c0 += RU) {
@@ -840,11 +845,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
               D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
             }
           }
+          constexpr int LG = S8 == 8 ? 4 : 2;  // lanes sharing a value after the scatter
           D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
-          const int vi = (lane >> 1) & (S8 - 1);  // rotated index of the value this lane holds
+          if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
+          const int vi = (lane / LG) & (S8 - 1);  // rotated index of the value this lane holds
           double* hb = hred + hpar * (NW * kWyHS + 16);
           hpar ^= 1;
-          if ((lane & 1) == 0) hb[warp * kWyHS + vi] = D[0];
+          if ((lane & (LG - 1)) == 0) hb[warp * kWyHS + vi] = D[0];
 #pragma unroll
           for (int e = 0; e < RPL; ++e)
             if (srow[e] == r) {
@@ -856,15 +863,16 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           WY_TR(12);
           double inv, wr;
           {
-            // every warp sums the NW partials of its value j = lane & 15 (fixed order) and forms the
-            // scalars; column (c0 + j) mod 16: > c update target, < c finished (column c of V^T V)
-            constexpr int WPP = NW / 2;
-            const int j = lane & 15, part = lane >> 4;
+            // every warp sums the NW partials of its value j = lane & (S8-1) (fixed order) and forms
+            // the scalars; column (c0 + j) mod S8: > c update target, < c finished (column c of V^T V)
+            constexpr int NP = 32 / S8, WPP = NW / NP;
+            const int j = lane & (S8 - 1), part = lane / S8;
             const double* hv = hb + part * WPP * kWyHS + j;
             double tot = 0.0;
 #pragma unroll
             for (int ww = 0; ww < WPP; ++ww) tot += hv[ww * kWyHS];
-            tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+#pragma unroll
+            for (int mb = S8; mb < 32; mb <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, mb);
             const double lam2 = __shfl_sync(0xffffffffu, tot, cj);
             const double u0 = hb[NW * kWyHS + cj];
             const double lam = sqrt(lam2);
@@ -874,10 +882,10 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             inv = nv2 > 0.0 ? rsqrt(nv2) : 0.0;  // identity reflector if lambda == 0 (R4)
             wr = u0 - diag;
             const double fv = 2.0 * inv * (tot - diag * hb[NW * kWyHS + j]);
-            const int col = (c0 + j) & 15;
-            if (lane < 16) wup[j] = col > c ? fv : 0.0;
+            const int col = (c0 + j) & (S8 - 1);
+            if (lane < S8) wup[j] = col > c ? fv : 0.0;
             if (warp == 0) {
-              if (lane < 16 && col < c) Gs[col + 16 * c] = 0.5 * fv;
+              if (lane < S8 && col < c) Gs[col + 16 * c] = 0.5 * fv;
               if (lane == 0) diagv[c] = diag;
             }
             __syncwarp();
@@ -902,7 +910,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           __syncwarp();  // wup is rewritten next round
         }
       }
-      // rotate by RU: column (c0 + RU + j) mod 16 to index j
+      // rotate by RU: column (c0 + RU + j) mod S8 to index j
 #pragma unroll
       for (int e = 0; e < RPL; ++e) {
         double tmp[S8];
