@@ -1295,9 +1295,13 @@ int pqr_laplacian7_apply(int nx, int ny, int nz, int s, const double* V, int64_t
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t work = npts * s;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 16, (work + 255) / 256));
-  k_laplacian7<<<grid, 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, s, V, ldv, Y, ldy);
+  // z-chunks so that the grid covers the SMs several times over (each chunk re-reads 2 halo planes)
+  const int64_t tiles = (int64_t)((nx + kLapTX - 1) / kLapTX) * ((ny + kLapTY - 1) / kLapTY);
+  if (tiles > INT32_MAX) return PQR_EARG;
+  int zchunk = nz;
+  while (zchunk > 8 && tiles * s * ((nz + zchunk - 1) / zchunk) < (int64_t)sms * 8) zchunk = (zchunk + 1) / 2;
+  const dim3 grid((unsigned)tiles, (unsigned)((nz + zchunk - 1) / zchunk), (unsigned)s);
+  k_laplacian7<<<grid, dim3(kLapTX, kLapTY), 0, (cudaStream_t)stream>>>(nx, ny, nz, zchunk, V, ldv, Y, ldy);
   return cudaGetLastError() == cudaSuccess ? PQR_OK : PQR_ECUDA;
 }
 

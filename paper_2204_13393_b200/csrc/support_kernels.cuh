@@ -4,29 +4,40 @@
 
 namespace pqr {
 
-// Y = A V, A = 7-point Dirichlet Laplacian (6 on the diagonal, -1 per existing neighbour).
-// One thread per grid point and column; x-neighbours are adjacent in memory so a warp's
-// loads are coalesced; the 6 neighbour reads hit L1/L2.
-__global__ void __launch_bounds__(256) k_laplacian7(int nx, int ny, int nz, int s, const double* __restrict__ V,
-                                                    int64_t ldv, double* __restrict__ Y, int64_t ldy) {
-  const int64_t npts = (int64_t)nx * ny * nz;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < npts * s; e += stride) {
-    const int c = (int)(e / npts);
-    const int64_t p = e - (int64_t)c * npts;
-    const int i = (int)(p % nx);
-    const int64_t jl = p / nx;
-    const int j = (int)(jl % ny);
-    const int l = (int)(jl / ny);
-    const double* v = V + (int64_t)c * ldv;
-    double acc = 6.0 * v[p];
-    if (i > 0) acc -= v[p - 1];
-    if (i + 1 < nx) acc -= v[p + 1];
-    if (j > 0) acc -= v[p - nx];
-    if (j + 1 < ny) acc -= v[p + nx];
-    if (l > 0) acc -= v[p - (int64_t)nx * ny];
-    if (l + 1 < nz) acc -= v[p + (int64_t)nx * ny];
-    Y[p + (int64_t)c * ldy] = acc;
+// Y = A V, A = 7-point Dirichlet Laplacian (6 on the diagonal, -1 per existing neighbour), the
+// operator of Block Arnoldi (configs[2]).  HBM-bound: each thread owns one
+// (x, y) line of one column and marches along z over a chunk of planes with the three z values in
+// registers (each point is read from HBM once); the x and y neighbours are loads of values the
+// same or a neighbouring warp loads in the same plane (L1 hits).  Blocks of 32 x 8 threads (x
+// along a warp: coalesced 256-byte rows); grid (x-tiles * y-tiles, z-chunks, columns).
+constexpr int kLapTX = 32, kLapTY = 8;
+__global__ void __launch_bounds__(kLapTX * kLapTY) k_laplacian7(int nx, int ny, int nz, int zchunk,
+                                                                 const double* __restrict__ V, int64_t ldv,
+                                                                 double* __restrict__ Y, int64_t ldy) {
+  const int tilesx = (nx + kLapTX - 1) / kLapTX;
+  const int i = (blockIdx.x % tilesx) * kLapTX + threadIdx.x;
+  const int j = (blockIdx.x / tilesx) * kLapTY + threadIdx.y;
+  const int c = blockIdx.z;
+  const int l0 = blockIdx.y * zchunk, l1 = min(nz, l0 + zchunk);
+  const bool in = i < nx && j < ny;
+  const int64_t plane = (int64_t)nx * ny;
+  const double* v = V + (int64_t)c * ldv + (int64_t)j * nx + i;
+  double* y = Y + (int64_t)c * ldy + (int64_t)j * nx + i;
+  double below = (in && l0 > 0) ? v[(int64_t)(l0 - 1) * plane] : 0.0;
+  double cur = in && l0 < nz ? v[(int64_t)l0 * plane] : 0.0;
+  for (int l = l0; l < l1; ++l) {
+    const double* vp = v + (int64_t)l * plane;
+    const double above = (in && l + 1 < nz) ? vp[plane] : 0.0;
+    if (in) {
+      double acc = 6.0 * cur - below - above;
+      if (i > 0) acc -= vp[-1];
+      if (i + 1 < nx) acc -= vp[1];
+      if (j > 0) acc -= vp[-nx];
+      if (j + 1 < ny) acc -= vp[nx];
+      y[(int64_t)l * plane] = acc;
+    }
+    below = cur;
+    cur = above;
   }
 }
 

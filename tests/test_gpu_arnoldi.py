@@ -69,15 +69,17 @@ def oracle_arnoldi(orc, R, nx, steps):
     return V, H[:k, :c0]
 
 
-def test_stencil_vs_numpy(P):
+@pytest.mark.parametrize("nx,ny,nz,s", [(9, 9, 9, 4), (37, 11, 23, 3), (64, 48, 40, 4), (1, 1, 5, 1), (33, 9, 300, 2)])
+def test_stencil_vs_numpy(P, nx, ny, nz, s):
+    """The operator kernel (z-marching lines, ragged x/y tiles, z chunks with halo planes)."""
     import torch
 
-    nx = 9
-    V = inputs.gaussian(3, nx ** 3, 4)
-    Y = empty(nx ** 3, 4)
-    P.pqr_laplacian7_apply(nx, nx, nx, 4, dev(V), Y)
+    n = nx * ny * nz
+    V = inputs.gaussian(3 + n, n, s)
+    Y = empty(n, s)
+    P.pqr_laplacian7_apply(nx, ny, nz, s, dev(V), Y)
     torch.cuda.synchronize()
-    assert rel(host(Y), lap7_numpy(V, nx, nx, nx)) < 1e-15
+    assert rel(host(Y), lap7_numpy(V, nx, ny, nz)) < 1e-15
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
