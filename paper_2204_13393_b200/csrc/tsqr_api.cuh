@@ -102,9 +102,15 @@ cudaError_t wy_up_g(const WyLevel& L, const WyPanels& P, int C, int s, int merge
   }
   if constexpr (NT == 1 && WM == 8) {  // panel merges only pair 4-wide panels (s = 4)
     if (merge) {
-      auto f = k_wy_up<UW, NT, WM, true, NG>;
+      auto f = k_wy_up<UW, NT, WM, true, NG, false, true>;
       ensure_smem(f, smem);
       f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, merge, mtoff);
+      return cudaGetLastError();
+    }
+    if (s <= 4) {  // narrow tail (4 register columns per row)
+      auto f = k_wy_up<UW, NT, WM, false, NG, false, true>;
+      ensure_smem(f, smem);
+      f<<<grid, kWyLaunch, smem, st>>>(L, P, C, s, 0, 0);
       return cudaGetLastError();
     }
   }

@@ -127,7 +127,7 @@ inline size_t wy_smem_bytes(int RP, int wmax, int cap, int nbuf, int NW, int NG)
 // CTA's blocks alternately (group g: its blocks jb = g, g + 2, ...), each with its own scratch
 // and named barrier; the producer streams the items in block order as for one group, so while
 // one group runs its block's Householder tail the other applies its panels.
-template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false, int NG = 1, bool CH = false>
+template <int NW, int UW, int NT, int WM, bool UP, bool MERGE = false, int NG = 1, bool CH = false, bool NAR = false>
 PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call, int ncol, int merge_,
                      int mtoff) {
   constexpr int NTH = 32 * NW, NLA = NTH * NG + 128;  // consumer threads per group, launch size
@@ -659,7 +659,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     //   v . x_c' = (D_c' - sigma*lambda x_c'[r]) / sqrt(...) for c' > c (the update), and
     //   v_c' . v_c by the same formula for c' < c (column c of V^T V, for T).
     constexpr int RPL = UW / 2;   // rows per lane in the row layout
-    constexpr int S8 = 8 * NT;    // columns per row
+    // columns per row (NAR: calls with s <= 4 — Arnoldi's blocks and every panel merge — keep 4)
+    static_assert(!NAR || NT == 1, "narrow tail: one 8-column tile");
+    constexpr int S8 = NAR ? 4 : 8 * NT;
     // Chained block: the tail's pivot rows C + c are the carry rows [C, C+s) (the chain's N so far;
     // no panel touches them).  They take the spare register rows [crow, crow + s) at the end of the
     // group's rows (chained blocks hold <= crow own rows) and join the rounds like own rows, with
@@ -707,7 +709,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
       for (int pb = 0; pb < 8; ++pb)
 #pragma unroll
-        for (int e = 0; e < RPL; ++e) xr[e][8 * nt + pb] = a[pb * RPL + e];
+        for (int e = 0; e < RPL; ++e)
+          if (8 * nt + pb < S8) xr[e][8 * nt + pb] = a[pb * RPL + e];
     }
     int rowk[RPL];  // block-local rows of this lane
 #pragma unroll
@@ -754,7 +757,7 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       }
     };
     WY_TR(10);
-    if constexpr (S8 == 8 && PQR_WY_ROT8 == 0) {
+    if constexpr (S8 <= 8 && PQR_WY_ROT8 == 0) {
 #pragma unroll
     for (int c = 0; c < S8; ++c) {
       if (c >= s) break;
@@ -779,9 +782,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
           D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
         }
       }
-      constexpr int LG = S8 == 8 ? 4 : 2;  // lanes sharing a value after the scatter
-      D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
-      if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
+      constexpr int LG = 32 / S8;  // lanes sharing a value after the scatter
+#pragma unroll
+      for (int m = 1; m < LG; m <<= 1) D[0] += __shfl_xor_sync(0xffffffffu, D[0], m);
       const int vi = (lane / LG) & (S8 - 1);
       double* hb = hred + hpar * (NW * kWyHS + 16);
       hpar ^= 1;
@@ -845,9 +848,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
               D[j] = keep + __shfl_xor_sync(0xffffffffu, send, mb);
             }
           }
-          constexpr int LG = S8 == 8 ? 4 : 2;  // lanes sharing a value after the scatter
-          D[0] += __shfl_xor_sync(0xffffffffu, D[0], 1);
-          if (LG == 4) D[0] += __shfl_xor_sync(0xffffffffu, D[0], 2);
+          constexpr int LG = 32 / S8;  // lanes sharing a value after the scatter
+#pragma unroll
+          for (int m = 1; m < LG; m <<= 1) D[0] += __shfl_xor_sync(0xffffffffu, D[0], m);
           const int vi = (lane / LG) & (S8 - 1);  // rotated index of the value this lane holds
           double* hb = hred + hpar * (NW * kWyHS + 16);
           hpar ^= 1;
@@ -1094,9 +1097,9 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 // Level kernels: NG groups of 16 / NG consumer warps (UW in 16-warp units, as planned by the
 // host).  NG = 2 when a CTA gets two or more blocks (one group's tail overlaps the other's
 // panels), NG = 1 (16 warps on one block: lower latency per block) for the small tree levels.
-template <int UW, int NT, int WM, bool MERGE, int NG, bool CH = false>
+template <int UW, int NT, int WM, bool MERGE, int NG, bool CH = false, bool NAR = false>
 __global__ void __launch_bounds__(kWyLaunch, 1) k_wy_up(WyLevel L, WyPanels P, int C, int s, int merge, int mtoff) {
-  wy_body<kWyWarps / NG, UW * NG, NT, WM, true, MERGE, NG, CH>(L, P, C, s, 0, 0, merge, mtoff);
+  wy_body<kWyWarps / NG, UW * NG, NT, WM, true, MERGE, NG, CH, NAR>(L, P, C, s, 0, 0, merge, mtoff);
 }
 
 // stage 2: Y_b = Q_b [coef; 0] (columns < t; columns t..ncol-1 zero)
