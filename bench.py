@@ -590,6 +590,7 @@ def run_arnoldi(args, rank, world, local_rank, device):
                 "config": {"workload": "arnoldi", "baseline_config": 2, "grid": g, "n_local": n, "s": s,
                            "pqr_calls": steps + 1, "k_range": [0, s * steps], "variants": variants,
                            "parallelism": f"replicas{world}", "operator_ms_per_step": op_ms,
+                           "pqr_plus_operator_ms_per_step": pqr_ms + op_ms,
                            "l2": "inputs exceed L2 (no flush needed)"},
                 "frac_of_roofline": (mand / world / (hbm * 1e9) * 1e3) / pqr_ms,
                 "kernel_share": {k: d["ms"] / tot for k, d in kinds.items()},

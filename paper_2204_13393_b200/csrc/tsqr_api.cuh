@@ -474,7 +474,8 @@ int tsqr_commit(Ctx* h, int s, int t, int merge = 0, int mtoff = 0) {
 int alloc_level(Ctx* h, TsqrLv& lv, int wmax, bool with_io) {
   TsqrState* ts = h->ts;
   int rc;
-  lv.UW = uw_for(lv.q + 2 * (lv.rem2 > 0) + lv.odd_last);
+  // (a chained leaf also holds the tail's s <= wmax carried pivot rows in its last register rows)
+  lv.UW = uw_for(lv.q + 2 * (lv.rem2 > 0) + lv.odd_last + (lv.chained ? wmax : 0));
   lv.RP = rp_for(lv.UW);
   if (lv.UW > 6 || (wmax > 8 && lv.UW > 2) || std::max(wy_smem(lv.RP, wmax, ts->cap, 2, 1), wy_smem(lv.RP, wmax, ts->cap, 2, 2)) > kWySmemBudget)
     return PQR_EPLAN;

@@ -77,6 +77,32 @@ def test_chains_vs_oracle(P, orc, sms, n, k0, widths, monkeypatch):
         assert np.array_equal(a["U"], b["U"]) and np.array_equal(a["N"], b["N"])
 
 
+@pytest.mark.parametrize("n,k0,widths,block_rows", [(138_329, 60, (1, 1), 512), (47_223, 21, (6, 6), 512),
+                                                    (60_001, 30, (16, 3), 256)])
+def test_chains_user_block_rows(P, orc, n, k0, widths, block_rows, monkeypatch):
+    """Chains with a user leaf size below the kernel's register capacity: the chained blocks' carried
+    pivot rows must still fit behind their own rows (regression: a 512-row leaf on an 8-column handle
+    overlapped them; found by tools/stress_parity.py)."""
+    import torch
+
+    monkeypatch.setenv("PQR_SMS", "2")
+    Q = inputs.orthonormal(801 + n % 7, n, k0)
+    Qcur = Q
+    with P.PQR(n, k0 + sum(widths), max(widths), dev(Q), k=k0, variant="tsqr", chains="on",
+               block_rows=block_rows) as h:
+        assert h.stats()["leaf_chains"] == 4
+        for i, s in enumerate(widths):
+            X = inputs.gaussian(810 + i, n, s)
+            U, Pm, Nm = empty(n, s), empty(Qcur.shape[1], s), empty(s, s)
+            t = h.solve(dev(X), U=U, P=Pm, N=Nm, s=s)
+            torch.cuda.synchronize()
+            ref = orc.householder_pqr(Qcur, X)
+            assert t == ref["t"]
+            assert rel(host(Pm), ref["P"]) < 1e-10 and rel(host(Nm), ref["N"]) < 1e-10
+            assert rel(host(U)[:, :t], ref["U"]) < 1e-10
+            Qcur = np.asfortranarray(np.hstack([Qcur, ref["U"]]))
+
+
 @pytest.mark.parametrize("n,k0,widths", [(40_000, 32, (8, 8)), (33_333, 20, (12, 4))])
 def test_chains_vs_tree(P, orc, n, k0, widths, monkeypatch):
     """Chains on and off are two locally orthogonal representations of the same basis: P, N, t and

@@ -53,13 +53,14 @@ def main():
         else:
             os.environ.pop("PQR_SMS", None)
         seed = int(rng.integers(1 << 30))
+        chains = "on" if variant == "tsqr" and rng.random() < 0.35 else "auto"  # FlatTSPQR leaves
         mode = ["plain", "plain", "append", "host", "dependent"][rng.integers(5)]
         Q = inputs.orthonormal(seed, n, k)
         try:
             nsolve = 3 if mode == "append" else 1
             ok, e, t = True, 0.0, None
             with pqr.PQR(n, k + (s * nsolve if mode == "append" else 0), s, dev(Q) if k else None, k=k,
-                         variant=variant, block_rows=br) as h:
+                         variant=variant, block_rows=br, chains=chains) as h:
                 Qcur = Q
                 for it in range(nsolve):
                     si = s if it == 0 else int(rng.integers(1, s + 1))
@@ -108,7 +109,7 @@ def main():
         cases += 1
         if not ok:
             fails += 1
-            print("FAIL", dict(mode=mode, variant=variant, n=n, k=k, s=s, block_rows=br, sms=sms,
+            print("FAIL", dict(mode=mode, variant=variant, n=n, k=k, s=s, block_rows=br, sms=sms, chains=chains,
                                nccl=os.environ.get("PQR_FORCE_NCCL"), seed=seed, t=t, err=e),
                   flush=True)
     print(f"stress_parity: {cases} cases, {fails} failures, {time.time() - t0:.0f} s")
