@@ -500,7 +500,7 @@ int tsqr_alloc(Ctx* h) {
   // node arity: even, node rows within the register/shared-memory budget
   const int rmax = wmax > 8 ? 512 : 1024;
   // node rows arity*cap <= rmax, even (paired 16-byte rows): odd arity only with even cap
-  ts->arity = std::max(2, std::min(8, rmax / cap));
+  ts->arity = std::max(2, std::min(64, rmax / cap));  // (8 before round 2: an extra level at small cap)
   if ((cap & 1) && (ts->arity & 1)) ts->arity -= 1;
   ts->arity = std::max(2, ts->arity);
   int rc;
