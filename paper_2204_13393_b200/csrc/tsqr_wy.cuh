@@ -723,7 +723,12 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
     int srow[RPL];
 #pragma unroll
     for (int e = 0; e < RPL; ++e)
+    {
       srow[e] = !chained ? rowk[e] : (rowk[e] < R ? (1 << 24) : (rowk[e] >= crow && rowk[e] - crow < s ? C + rowk[e] - crow : -1));
+      // opaque to the compiler: otherwise it specialises the whole unrolled tail for srow == rowk
+      // (unchained blocks) and keeps two copies of it (+3 K instructions: instruction-cache misses)
+      if constexpr (CH) asm volatile("" : "+r"(srow[e]));
+    }
     double* Gs = tsc;  // strict upper part of V^T V (ld 16), column c written in round c by tid 0
     // Round scalars, formed by every warp from the NW warp partials of hb (the same fixed summation
     // order in every warp and lane: bitwise-identical values), so a round needs one barrier:
@@ -1064,16 +1069,25 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         // panel) from the carry register rows, and the carry parts of the new reflectors (rows
         // [C + c, C + s) of column C + c) into their segments [xs, xs + LS), xs = (C + c) & ~1;
         // warp 0 writes the segments' zero entries
+        // (through ctl and a compact loop: the carry rows are the last warp's; an unrolled
+        // per-register store loop here cost 2.7 K instructions of instruction cache)
+        if (warp == NW - 1) {
 #pragma unroll
-        for (int e = 0; e < RPL; ++e) {
-          const int sr = srow[e];
-          if (sr >= C && sr < C + s) {
+          for (int e = 0; e < RPL; ++e) {
+            const int sr = srow[e];
+            if (sr >= C && sr < C + s) {
 #pragma unroll
-            for (int c = 0; c < S8; ++c) {
-              if (c >= s) break;
-              st_l2pol(kslot + sr + (int64_t)c * kld, sr < C + c ? xr[e][c] : (sr == C + c ? diagv[c] : 0.0), kpol);
-              const int xs = (C + c) & ~1;
-              if (sr >= C + c) L.VC[(b * L.cap + C + c) * LS + sr - xs] = xr[e][c];
+              for (int c = 0; c < S8; ++c) ctl[(sr - C) * S8 + c] = xr[e][c];
+            }
+          }
+          __syncwarp();
+#pragma unroll 1
+          for (int e = lane; e < s * S8; e += 32) {
+            const int i = e / S8, c = e % S8;
+            if (c < s) {
+              const double v = ctl[e];
+              st_l2pol(kslot + C + i + (int64_t)c * kld, i < c ? v : (i == c ? diagv[c] : 0.0), kpol);
+              if (i >= c) L.VC[(b * L.cap + C + c) * LS + C + i - ((C + c) & ~1)] = v;
             }
           }
         }
