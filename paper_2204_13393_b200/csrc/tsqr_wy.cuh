@@ -110,9 +110,9 @@ PQR_DEV int wy_rows(const WyLevel& L, int64_t b) {
 
 // per-group scratch (doubles) of a level kernel with NW consumer warps per group:
 // partials (NW + 1) E, Z (E), Householder-round buffers, diag, T scratch, round coefficients,
-// a chained block's carry rows: the stage-1 tail's (E) and two panels' (2 E)
+// a chained block's carry rows: the stage-1 tail's (E) and three panels' (3 E)
 PQR_HOST_DEV constexpr int wy_group_scratch(int NW, int E) {
-  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 64 + 3 * E;
+  return (NW + 1) * E + E + 2 * (NW * kWyHS + 16) + 16 + 512 + 4 * E;
 }
 // ring slot (doubles): a panel (RP x wm), its T (wm x wm), its columns' carry segments (wm x LS)
 PQR_HOST_DEV constexpr int wy_slot(int RP, int wm) { return RP * wm + wm * wm + wm * (wm + 2); }
@@ -149,9 +149,8 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
   double* hred = Zs + E;                   // 2 x (NW*17 partials + 16 pivot-row values)
   double* diagv = hred + 2 * (NW * kWyHS + 16);  // 16: sigma*lambda of the new columns
   double* tsc = diagv + 16;                // 2 x 16 x 16: V^T V of the new panel, T-column scratch
-  double* hfc = tsc + 512;                 // 2 x 32: Householder-round coefficients (by round parity)
-  double* ctl = hfc + 64;                  // E: carry rows [C, C+s) of a chained block's tail (row-major, ld 8*NT)
-  double* kbuf = ctl + E;                  // 2 x E: K[x : x+w, :] of a chained block's panels (ld wm), by panel parity
+  double* ctl = tsc + 512;                 // E: carry rows [C, C+s) of a chained block's tail (row-major, ld 8*NT)
+  double* kbuf = ctl + E;                  // 3 x E: K[x : x+w, :] of a chained block's panels (ld wm), panel p at p % 3
   // NW x 16 per-warp round coefficients of the 16-column tail: the T-column half of tsc, which the
   // rounds leave free (T is formed after them)
   double* hupd = tsc + 256;
@@ -314,13 +313,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       if (xw) cbar();
       else __syncwarp();
     }
-    // chained block, warp 0: K rows of panel p into kbuf[p & 1] by cp.async, one commit group per
-    // panel (panel p + 1's rows are fetched while panel p runs; a panel's rows are disjoint from
+    // chained block, warp 0: K rows of panel p into kbuf[p % 3] by cp.async, one commit group per
+    // panel (panel p + 2's rows are fetched while panel p runs; a panel's rows are disjoint from
     // every other panel's, so the prefetch never reads a row an earlier panel rewrites)
     auto kfetch = [&](int pp) {
       if (pp < np) {
         const int4 pn = pans[UP ? pp : np - 1 - pp];
-        double* dst = kbuf + (pp & 1) * E;
+        double* dst = kbuf + (pp % 3) * E;
         for (int e = lane; e < wm * s; e += 32) {
           const int i = e % wm, c = e / wm;  // (rows i >= w are never read)
           if (i < pn.y) cp_async8_l2pol(dst + i + wm * c, kslot + pn.x + i + (int64_t)c * kld, kpol);
@@ -336,7 +335,10 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       }
       cp_async_commit();
     }
-    if (chained && warp == 0) kfetch(0);
+    if (chained && warp == 0) {
+      kfetch(0);
+      kfetch(1);
+    }
     double x[UW][NT][4];
     if (UP) {
       WY_TR(9);
@@ -394,11 +396,11 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
       auto vcar = [&](int r, int j) -> double {
         return (j < w && r >= px + j && r < px + w) ? vcs[j * LS + r - ((px + j) & ~1)] : 0.0;
       };
-      const double* kb = kbuf + (p & 1) * E;  // K[px + i][c] at kb[i + wm c]
-      if (kw) kfetch(p + 1);
+      const double* kb = kbuf + (p % 3) * E;  // K[px + i][c] at kb[i + wm c]
+      if (kw) kfetch(p + 2);
       // this panel's K rows have landed (waited for right before their first use)
       auto kready = [&]() {
-        cp_async_wait<1>();
+        cp_async_wait<2>();
         __syncwarp();
       };
       // K[px + 4kk + q][8nt + g] (zero outside the panel's rows and the block's columns)
@@ -439,6 +441,13 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
+        if (kw) {  // + K[px:px+w]^T Vc (rows px + 4kk + q), first: the unit MMAs hide its latency
+          kready();
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) dmma884(acc[kk][nt][0], acc[kk][nt][1], kcar(nt, kk), vcar(px + 4 * kk + q, g));
+        }
 #pragma unroll
         for (int u = 0; u < UW; ++u) {
           const int row = 16 * (warp * UW + u) + 4 * q;
@@ -453,13 +462,6 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
             dmma884(ac[0], ac[1], x[u][nt][2], a23.x);
             dmma884(ac[0], ac[1], x[u][nt][3], a23.y);
           }
-        }
-        if (kw) {  // + K[px:px+w]^T Vc (rows px + 4kk + q)
-          kready();
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) dmma884(acc[kk][nt][0], acc[kk][nt][1], kcar(nt, kk), vcar(px + 4 * kk + q, g));
         }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -506,6 +508,14 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
 #pragma unroll
       for (int mt = 0; mt < MTM; ++mt) {
         if (mt < mtn) {
+          if (kw) {  // + Vc^T K[px:px+w] (rows px + 4kk + q), before the unit MMAs
+            if (mt == 0) kready();
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                dmma884(acc[kk & 1][mt][nt][0], acc[kk & 1][mt][nt][1], vcar(px + 4 * kk + q, 8 * mt + g), kcar(nt, kk));
+          }
 #pragma unroll
           for (int u = 0; u < UW; ++u) {
             const int row = 16 * (warp * UW + u) + 4 * q;
@@ -520,14 +530,6 @@ PQR_DEV void wy_body(const WyLevel& L, const WyPanels& P, int C, int s, int Call
               dmma884(ac[0], ac[1], a23.x, x[u][nt][2]);
               dmma884(ac[0], ac[1], a23.y, x[u][nt][3]);
             }
-          }
-          if (kw) {  // + Vc^T K[px:px+w] (rows px + 4kk + q)
-            if (mt == 0) kready();
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                dmma884(acc[kk & 1][mt][nt][0], acc[kk & 1][mt][nt][1], vcar(px + 4 * kk + q, 8 * mt + g), kcar(nt, kk));
           }
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
