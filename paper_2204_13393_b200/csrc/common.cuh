@@ -202,8 +202,9 @@ namespace pqr {
 // column-major m x s each, at partials + b*ms).  Partial b goes to accumulator b % 4, the four
 // are combined as (a0 + a1) + (a2 + a3): a fixed order, so results are bitwise reproducible.
 // 16 independent L2 loads per thread are in flight per step (the reduction is latency-bound).
-PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, double* W, int ldw) {
-  for (int e = threadIdx.x; e < ms; e += blockDim.x) {
+PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, double* W, int ldw, int tid,
+                               int nthr) {
+  for (int e = tid; e < ms; e += nthr) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     int b = 0;
     for (; b + 16 <= nb; b += 16) {
@@ -221,6 +222,9 @@ PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, do
     const int jj = e % m, c = e / m;
     W[jj + (int64_t)c * ldw] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   }
+}
+PQR_DEV void grid_sum_partials(const double* partials, int nb, int ms, int m, double* W, int ldw) {
+  grid_sum_partials(partials, nb, ms, m, W, ldw, threadIdx.x, blockDim.x);
 }
 }  // namespace pqr
 

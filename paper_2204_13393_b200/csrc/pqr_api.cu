@@ -518,7 +518,18 @@ int run_s2(int mode, const S2Args& a0, int sms, cudaStream_t st, int64_t* launch
                    (!a0.U2 || ((a0.ldu2 & 1) == 0 && aligned16(a0.U2)));
   if (!vec) return PQR_EPLAN;
   S2Args a = a0;
-  a.nslot = s2_nslot(MT, NT, mode, kSmemBudget);
+  // warp-specialised fused pass (a producer warpgroup issues the slot copies): faster with two
+  // output tiles (config D, s = 16: 1.10 -> 1.00 ms), slower with one (weak config: 8.3-8.4 ->
+  // 8.8-8.9 ms; configs[1]: 1.99 -> 2.21 ms; tools/ws_ab.sh); PQR_S2_WS=0|1 forces
+  static const int env_ws = getenv("PQR_S2_WS") ? atoi(getenv("PQR_S2_WS")) : -1;
+  a.ws = mode == kS2Fused && (env_ws >= 0 ? env_ws > 0 : NT == 2) ? 1 : 0;
+  a.nslot = s2_nslot(MT, NT, mode, kSmemBudget, a.ws != 0);
+  // slot cap: with 17 one-tile columns groups (weak config) 12 slots beat the 13 that fit
+  // (fused pass 8.30-8.42 -> 7.82-7.99 ms, 3 interleaved pairs; 10 and 11: 7.85 / 7.97), while
+  // configs[1] (MT = 9) wants all 24 (12: 1.97 -> 2.04 ms; tools/nsl_ab.sh).  PQR_S2_NSL caps (A/B)
+  static const int env_nsl = getenv("PQR_S2_NSL") ? atoi(getenv("PQR_S2_NSL")) : -1;
+  const int cap = env_nsl >= 0 ? env_nsl : (mode == kS2Fused && NT == 1 && MT >= 16 && !a.ws ? 12 : 0);
+  if (cap > 0) a.nslot = std::min(a.nslot, cap);
   // refill copies interleaved with the G phase: faster up to 12 tiles (config S: 2.14 -> 1.95 ms),
   // slower at 17 (weak config: 7.7 -> 9.3 ms); PQR_S2_IL=0|1 forces
   static const int env_il = getenv("PQR_S2_IL") ? atoi(getenv("PQR_S2_IL")) : -1;

@@ -4,14 +4,18 @@
 using namespace pqr;
 
 namespace {
-template <int MT, int NT>
-cudaError_t go(const S2Args& a, int grid, cudaStream_t st) {
-  auto f = k_stream2<MT, NT, kS2Fused>;
-  const size_t smem = s2_smem(MT, NT, kS2Fused, a.nslot);
+template <int MT, int NT, bool WS>
+cudaError_t go_t(const S2Args& a, int grid, cudaStream_t st) {
+  auto f = k_stream2<MT, NT, kS2Fused, WS>;
+  const size_t smem = s2_smem(MT, NT, kS2Fused, a.nslot, WS);
   const cudaError_t e = ensure_smem(f, smem);
   if (e != cudaSuccess) return e;
-  f<<<grid, kS2Threads, smem, st>>>(a);
+  f<<<grid, WS ? kS2WsThreads : kS2Threads, smem, st>>>(a);
   return cudaGetLastError();
+}
+template <int MT, int NT>
+cudaError_t go(const S2Args& a, int grid, cudaStream_t st) {
+  return a.ws ? go_t<MT, NT, true>(a, grid, st) : go_t<MT, NT, false>(a, grid, st);
 }
 }  // namespace
 

@@ -45,6 +45,10 @@ namespace pqr {
 #endif
 constexpr int kS2Consumers = 8;
 constexpr int kS2Threads = 32 * kS2Consumers;
+// warp-specialised form (S2Args::ws): + one producer warpgroup that issues every slot copy;
+// setmaxnreg splits the launch allocation (384 x 168): 256 x 216 + 128 x 72 <= 384 x 168
+constexpr int kS2WsThreads = kS2Threads + 128;
+constexpr int kS2WsConsumerRegs = 216, kS2WsProducerRegs = 72;
 constexpr int kS2Rows = 16;
 constexpr int kS2Gram = 1, kS2Update = 2, kS2Fused = 3;
 
@@ -64,12 +68,17 @@ struct S2Args {
   int interleave;                   // fused: refill copies interleaved with the G phase (else after it)
   int pf_rounds;                    // L2 prefetch distance in rounds of 8 units (0: off)
   int issue_loop;                   // copies issued by a loop over the lane's columns (else unrolled)
+  int ws;                           // warp-specialised launch (k_stream2<..., true>, kS2WsThreads)
 };
 
 PQR_HOST_DEV int s2_swz(int j) { return 3 * (j & 1) + 4 * ((j >> 1) & 1); }
 
-template <int MT, int NT, int MODE>
-__global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
+// WS: the copies are issued by a producer warpgroup (warps 8..11, slot sl by producer warp sl % 4)
+// instead of the consuming warp; a consumer releases its slot through the slot's `empty` mbarrier
+// (one arrival), and the producer waits on it before the slot's next fill.  The consumer warps
+// then issue only their LDS / DMMA / store stream.
+template <int MT, int NT, int MODE, bool WS = false>
+__global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S2Args a) {
   constexpr bool DO_U = (MODE & kS2Update) != 0, DO_G = (MODE & kS2Gram) != 0;
   constexpr int MP = MT * 8, SLOT = MP * kS2Rows;  // doubles per slot
   // two output tiles (NT = 2): the M fragments live in shared memory (in registers they would
@@ -80,18 +89,20 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
   const int k = a.k, m = k + a.sx, NSL = a.nslot;
   double* sMf = sm + (size_t)NSL * SLOT;  // [2MT][NT][32 lanes] (MSMEM)
   uint64_t* full = reinterpret_cast<uint64_t*>(sMf + MFS);
-  volatile int* fills = reinterpret_cast<volatile int*>(full + NSL);  // fills issued per slot
+  uint64_t* empty = full + NSL;  // WS: slot released by its consumer (one arrival)
+  volatile int* fills = reinterpret_cast<volatile int*>(full + (WS ? 2 : 1) * NSL);  // fills issued per slot
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
 
   // slot columns m..MP-1 are never copied: zero them once (finite operands, zero products)
-  for (int e = tid; e < NSL * (MP - m) * kS2Rows; e += kS2Threads) {
+  for (int e = tid; e < NSL * (MP - m) * kS2Rows; e += (WS ? kS2WsThreads : kS2Threads)) {
     const int sl = e / ((MP - m) * kS2Rows), r = e % ((MP - m) * kS2Rows);
     sm[(size_t)sl * SLOT + m * kS2Rows + r] = 0.0;
   }
   if (tid == 0) {
     for (int i = 0; i < NSL; ++i) {
       mbar_init(&full[i], 32);
+      if constexpr (WS) mbar_init(&empty[i], 1);
       fills[i] = 0;
     }
     fence_mbar_init();
@@ -150,7 +161,42 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
     }
     publish(sl, f);
   };
-  for (int i = warp; i < nu && i < NSL; i += kS2Consumers) issue(i, i, 0);
+  // consumer-side CTA barrier (WS: the producer warps have left; named barrier 1 over the consumers)
+  auto csync = [&]() {
+    if constexpr (WS) asm volatile("bar.sync 1, %0;\n" ::"n"(kS2Threads) : "memory");
+    else __syncthreads();
+  };
+  if constexpr (WS) {
+    if (warp >= kS2Consumers) {
+      // ---------------- producer warps: every fill of every slot, in unit order ----------------
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kS2WsProducerRegs));
+      // producer warp pw owns slots pw, pw + 4, ...: all fills of a slot come from one warp, in
+      // order, so the empty barrier's phase is never more than one behind (no parity aliasing)
+      bool done = false;
+      for (int f = 0; !done; ++f)
+        for (int sl = warp - kS2Consumers; sl < NSL; sl += 4) {
+          const int i = f * NSL + sl;
+          if (i >= nu) {
+            done = true;
+            break;
+          }
+          if (f > 0) mbar_wait(&empty[sl], (uint32_t)((f - 1) & 1));
+          const int64_t row = unit_row(i);
+          const int bytes = row_bytes(row);
+          double* d = sm + (size_t)sl * SLOT + dsto;
+          const double* src = a.Q + (int64_t)cp_jl * a.ldq + row;
+          int t = 0;
+          for (; t < nq; ++t, src += 4 * a.ldq) cp_async16(d + t * 64, bytes ? src : safe, bytes);
+          src = a.X + (int64_t)(cp_jl + 4 * nq - k) * a.ldx + row;
+          for (int e = 0; e < nx; ++e, ++t, src += 4 * a.ldx) cp_async16(d + t * 64, bytes ? src : safe, bytes);
+          publish(sl, f);
+        }
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kS2WsConsumerRegs));
+  } else {
+    for (int i = warp; i < nu && i < NSL; i += kS2Consumers) issue(i, i, 0);
+  }
   {
     // ---------------- consumer warps ----------------
     double mreg[(DO_U && !MSMEM) ? 2 * MT : 1][NT];
@@ -166,7 +212,7 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
           mreg[kk][nt] = v;
         }
       }
-    if constexpr (MSMEM) __syncthreads();
+    if constexpr (MSMEM) csync();
     const int tv = a.t_dev ? *a.t_dev : a.sout;
     const int offU = q * kS2Rows + 2 * (g ^ s2_swz(q));  // column 4kk+q, pair g (+ kk*64)
     const int sg = s2_swz(g & 3);
@@ -279,7 +325,7 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
       }
       // fused pass: the refill of this slot with unit i + NSL is interleaved with the G phase,
       // tile by tile, each tile's copies behind the MMAs that consumed its last reads
-      const bool refill = MODE == kS2Fused && a.interleave && i + NSL < nu;
+      const bool refill = !WS && MODE == kS2Fused && a.interleave && i + NSL < nu;
       const uint32_t rdst = sm0 + 8u * (uint32_t)(sl * SLOT);
       const int64_t rrow = unit_row(i + NSL);
       const int rbytes = row_bytes(rrow);
@@ -346,7 +392,11 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
           }
         }
       }
-      if (refill) {
+      if constexpr (WS) {
+        // every lane's reads of the slot have completed (their MMAs have issued): release it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sl]);
+      } else if (refill) {
         publish(sl, f + 1);
       } else if (!(MODE == kS2Fused && a.interleave) && i + NSL < nu) {
         // every lane's reads of the slot have completed (their MMAs have issued): refill it
@@ -361,7 +411,7 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
   }
   if constexpr (DO_G) {
     // ---- CTA reduction over the 8 warps (fixed order), then over the CTAs ----
-    __syncthreads();
+    csync();
     constexpr int PW = MT * NT * 64;  // doubles per warp
     double* red = sm;
     {
@@ -373,7 +423,7 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
           red[warp * PW + ((mt * NT + nt) * 32 + lane) * 2 + 1] = acc[mt][nt][1];
         }
     }
-    __syncthreads();
+    csync();
     double* part = a.partials + (size_t)blockIdx.x * m * a.sx;
     for (int e = tid; e < PW; e += kS2Threads) {
       const int v = e & 1, l = (e >> 1) & 31, rest = e >> 6;
@@ -387,13 +437,13 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
       }
     }
     __threadfence();
-    __syncthreads();
+    csync();
     __shared__ unsigned int s_last;
     if (tid == 0) s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
-    __syncthreads();
+    csync();
     if (!s_last) return;
     __threadfence();
-    grid_sum_partials(a.partials, gridDim.x, m * a.sx, m, a.W, a.ldw);
+    grid_sum_partials(a.partials, gridDim.x, m * a.sx, m, a.W, a.ldw, tid, kS2Threads);
     if (tid == 0) *a.ticket = 0u;
   }
 }
@@ -404,13 +454,13 @@ __global__ void __launch_bounds__(kS2Threads, 1) k_stream2(S2Args a) {
 inline size_t s2_mfs(int MT, int NT, int mode) {
   return (NT == 2 && (mode & kS2Update)) ? (size_t)2 * MT * NT * 32 * sizeof(double) : 0;
 }
-inline int s2_nslot(int MT, int NT, int mode, size_t budget) {
-  const size_t slot = (size_t)MT * 8 * kS2Rows * sizeof(double) + sizeof(uint64_t) + sizeof(int);
+inline int s2_nslot(int MT, int NT, int mode, size_t budget, bool ws = false) {
+  const size_t slot = (size_t)MT * 8 * kS2Rows * sizeof(double) + (ws ? 2 : 1) * sizeof(uint64_t) + sizeof(int);
   return (int)std::min<size_t>(24, (budget - 1024 - s2_mfs(MT, NT, mode)) / slot);
 }
-inline size_t s2_smem(int MT, int NT, int mode, int nslot) {
+inline size_t s2_smem(int MT, int NT, int mode, int nslot, bool ws = false) {
   return (size_t)nslot * MT * 8 * kS2Rows * sizeof(double) + s2_mfs(MT, NT, mode) +
-         (size_t)nslot * (sizeof(uint64_t) + sizeof(int));
+         (size_t)nslot * ((ws ? 2 : 1) * sizeof(uint64_t) + sizeof(int));
 }
 
 }  // namespace pqr
