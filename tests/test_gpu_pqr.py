@@ -132,6 +132,25 @@ def test_deflation_small(P, orc, variant):
     assert rel(Pu, Pr) < 1e-6
 
 
+def test_deflation_small_tsqr_columnwise(P, orc):
+    """configs[3] shape, TSQR (Householder) variant: the grading of X is a column scaling, and
+    Householder QR is column-wise backward stable (its Q factor and each column's relative error
+    do not depend on the column scales), so every kept column of U and every column of [P; N]
+    matches the oracle's Householder QR relative to that column's own norm — not only through
+    the 1e-6 projector of test_deflation_small (reading R11 bounds only the Cholesky variant)."""
+    Q, X = inputs.deflation_inputs(51, 2 ** 15, 96, 16)
+    ref = orc.householder_pqr(Q, X)
+    out = solve(P, Q, X, variant="tsqr")
+    t = ref["t"]
+    assert out["t"] == t == 14
+    errs_u = [np.linalg.norm(out["U"][:, j] - ref["U"][:, j]) for j in range(t)]  # unit columns
+    assert max(errs_u) < 1e-9, errs_u
+    for j in range(16):
+        cref = np.concatenate([ref["P"][:, j], ref["N"][:, j]])
+        cout = np.concatenate([out["P"][:, j], out["N"][:, j]])
+        assert np.linalg.norm(cout - cref) < 1e-10 * np.linalg.norm(cref), j
+
+
 def test_cholqr2_single_pass_is_bcgs_pip(P, orc):
     """PQR_SINGLE_PASS = Alg. 7 (one BCGS-PIP pass): same result as the oracle's Alg. 7."""
     Q, X = inputs.projected_inputs(61, 20_000, 32, 4, ratio=1e-2)
