@@ -538,9 +538,6 @@ int run_s2(int mode, const S2Args& a0, int sms, cudaStream_t st, int64_t* launch
   a.issue_loop = env_lp;
   a.interleave = env_il >= 0 ? env_il : (MT <= 12 ? 1 : 0);
   a.pf_rounds = env_pf;
-  // deferred refill (fused, not warp-specialised, not interleaved): PQR_S2_DEFER=0|1 forces
-  static const int env_df = getenv("PQR_S2_DEFER") ? atoi(getenv("PQR_S2_DEFER")) : -1;
-  a.defer = mode == kS2Fused && !a.ws && !a.interleave && (env_df >= 0 ? env_df > 0 : false) ? 1 : 0;
   if (a.nslot < kS2Consumers + 1) return PQR_EPLAN;
   const int64_t nunits = (a.n + kS2Rows - 1) / kS2Rows;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, nunits));

@@ -69,7 +69,6 @@ struct S2Args {
   int pf_rounds;                    // L2 prefetch distance in rounds of 8 units (0: off)
   int issue_loop;                   // copies issued by a loop over the lane's columns (else unrolled)
   int ws;                           // warp-specialised launch (k_stream2<..., true>, kS2WsThreads)
-  int defer;                        // fused: a freed slot's refill copies are issued inside the U phase of the warp's next unit
 };
 
 PQR_HOST_DEV int s2_swz(int j) { return 3 * (j & 1) + 4 * ((j >> 1) & 1); }
@@ -230,19 +229,6 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
       offB1[nt] = jc * kS2Rows + 2 * ((2 * q + 1) ^ s2_swz(jc));
     }
     int sl = warp, f = 0;  // slot and fill of unit i (i = f * NSL + sl)
-    // deferred refill (fused, a.defer): the refill of the slot a warp has just consumed is not
-    // issued as a loop after the G phase (34 LDGSTS with a dependent address update and a taken
-    // branch each: a quarter of the kernel's stall samples, with no DMMA of this warp in flight)
-    // but one copy per k-step inside the U phase of the warp's NEXT unit, in the shadow of its
-    // DMMAs.  The slot is free by then (no hazard); fill i + NSL then depends on the arrival of
-    // unit i + 8 instead of the completion of unit i, a chain that still walks back to the
-    // initial fills, so it cannot deadlock.
-    constexpr bool DEFER = MODE == kS2Fused && !WS;
-    bool pend = false;
-    uint32_t pdst = 0;
-    const double *psq = safe, *psx = safe;
-    int pbytes = 0, psl = 0, pf = 0;
-    const int64_t q4 = 4 * a.ldq, x4 = 4 * a.ldx;
     // L2 prefetch: round r = units 8r..8r+7 of this CTA (128 contiguous rows); warp (r % 8)
     // prefetches round r + pf_rounds when it starts its unit of round r (one bulk L2 prefetch of
     // the round's rows per column, spread over the lanes): the slot copies then hit L2
@@ -294,19 +280,6 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
             else mv = mreg[kk][nt];
             dmma884(dx[nt][kk % UC][0], dx[nt][kk % UC][1], mv, b.x);
             dmma884(dy[nt][kk % UC][0], dy[nt][kk % UC][1], mv, b.y);
-          }
-          if constexpr (DEFER) {
-            if (pend) {  // copy kk of the pending refill (columns cp_jl + 4kk)
-              const double* src = kk < nq ? psq + kk * q4 : psx + (kk - nq) * x4;
-              const int nb = kk < nq + nx ? pbytes : 0;
-              cp_async16_s(pdst + 512u * kk, nb ? src : safe, nb);
-            }
-          }
-        }
-        if constexpr (DEFER) {
-          if (pend) {
-            publish(psl, pf);
-            pend = false;
           }
         }
         const int64_t row = (ub + i) * kS2Rows + 4 * q;
@@ -425,17 +398,6 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
         if (lane == 0) mbar_arrive(&empty[sl]);
       } else if (refill) {
         publish(sl, f + 1);
-      } else if (DEFER && a.defer) {
-        if (i + NSL < nu) {
-          const int64_t row = unit_row(i + NSL);
-          pbytes = row_bytes(row);
-          pdst = sm0 + 8u * (uint32_t)(sl * SLOT);
-          psq = a.Q + (int64_t)cp_jl * a.ldq + row;
-          psx = a.X + (int64_t)(cp_jl + 4 * nq - k) * a.ldx + row;
-          psl = sl;
-          pf = f + 1;
-          pend = true;
-        }
       } else if (!(MODE == kS2Fused && a.interleave) && i + NSL < nu) {
         // every lane's reads of the slot have completed (their MMAs have issued): refill it
         issue(i + NSL, sl, f + 1);
