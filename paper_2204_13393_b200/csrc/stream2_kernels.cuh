@@ -40,6 +40,9 @@ namespace pqr {
 #ifndef PQR_S2_UCH
 #define PQR_S2_UCH 2  // U-phase accumulator chains per row half (2 or 4)
 #endif
+#ifndef PQR_S2_CPUNROLL
+#define PQR_S2_CPUNROLL 0  // unroll factor of the slot-copy issue loop (0: the compiler's choice; A/B: tools/cpunroll_ab.sh)
+#endif
 #ifndef PQR_S2_TG
 #define PQR_S2_TG 2  // G-phase tile group (1: each tile's four k-steps back to back; measured best: 2)
 #endif
@@ -152,6 +155,10 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
       double* d = sm + (size_t)sl * SLOT + dsto;
       const double* src = a.Q + (int64_t)cp_jl * a.ldq + row;
       int t = 0;
+#if PQR_S2_CPUNROLL > 0
+      constexpr int kCpUnroll = PQR_S2_CPUNROLL;
+#pragma unroll kCpUnroll
+#endif
       for (; t < nq; ++t, src += 4 * a.ldq) cp_async16(d + t * 64, bytes ? src : safe, bytes);
       src = a.X + (int64_t)(cp_jl + 4 * nq - k) * a.ldx + row;
       for (int e = 0; e < nx; ++e, ++t, src += 4 * a.ldx) cp_async16(d + t * 64, bytes ? src : safe, bytes);
