@@ -531,12 +531,11 @@ int run_s2(int mode, const S2Args& a0, int sms, cudaStream_t st, int64_t* launch
   const int cap = env_nsl >= 0 ? env_nsl : (mode == kS2Fused && NT == 1 && MT >= 16 && !a.ws ? 12 : 0);
   if (cap > 0) a.nslot = std::min(a.nslot, cap);
   // refill copies interleaved with the G phase: faster up to 12 tiles (config S: 2.14 -> 1.95 ms),
-  // slower at 17 (weak config: 7.7 -> 9.3 ms); PQR_S2_IL=0|1 forces
+  // slower at 17 (weak config: 7.7 -> 9.3 ms), so the kernel compiles it out past
+  // kS2InterleaveMaxMT tiles; PQR_S2_IL=0 disables it below
   static const int env_il = getenv("PQR_S2_IL") ? atoi(getenv("PQR_S2_IL")) : -1;
   static const int env_pf = getenv("PQR_S2_PF") ? atoi(getenv("PQR_S2_PF")) : 0;
-  static const int env_lp = getenv("PQR_S2_LOOP") ? atoi(getenv("PQR_S2_LOOP")) : 1;
-  a.issue_loop = env_lp;
-  a.interleave = env_il >= 0 ? env_il : (MT <= 12 ? 1 : 0);
+  a.interleave = MT <= kS2InterleaveMaxMT && (env_il >= 0 ? env_il != 0 : true) ? 1 : 0;
   a.pf_rounds = env_pf;
   if (a.nslot < kS2Consumers + 1) return PQR_EPLAN;
   const int64_t nunits = (a.n + kS2Rows - 1) / kS2Rows;

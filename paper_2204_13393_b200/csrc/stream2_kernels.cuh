@@ -43,6 +43,27 @@ namespace pqr {
 #ifndef PQR_S2_CPUNROLL
 #define PQR_S2_CPUNROLL 0  // unroll factor of the slot-copy issue loop (0: the compiler's choice; A/B: tools/cpunroll_ab.sh)
 #endif
+#ifndef PQR_S2_PF
+#define PQR_S2_PF 0  // 1: compile the L2 prefetch of later rounds in (S2Args::pf_rounds; measured: no gain)
+#endif
+#ifndef PQR_S2_GBAR
+// what separates the G phase's tile groups when the interleaved refill is compiled out (MT > 12):
+// 0 nothing (one basic block), 1 a compiler-level memory barrier, 2 the run-time refill test as
+// below 12 tiles (a never-taken-path branch per group).  Measured equal (with PQR_S2_KTEST = 0);
+// 2 keeps the code closest to the tuned build
+#define PQR_S2_GBAR 2
+#endif
+#ifndef PQR_S2_KTEST
+// 1: every G-phase tile selects its A operand at run time (slot column, or U column through
+// shuffles, by 8 mt + 8 <= k); 0: tiles below MT - NT - 1, Q columns for every k, skip the test
+// and its shuffles.  Measured (tools/gbar_ab.sh, profiles/r02m_gbar_ab.txt): 0 drops 120 SHFL per
+// unit but the weak config's fused pass goes 7.6-7.7 -> 9.1-9.2 ms (ptxas then schedules the tile
+// loads differently); configs[1] is the same either way.  So 1.
+#define PQR_S2_KTEST 1
+#endif
+#ifndef PQR_S2_LOOP
+#define PQR_S2_LOOP 1  // slot copies issued by a loop over the lane's columns (0: fully unrolled, fresh addresses)
+#endif
 #ifndef PQR_S2_TG
 #define PQR_S2_TG 2  // G-phase tile group (1: each tile's four k-steps back to back; measured best: 2)
 #endif
@@ -54,6 +75,7 @@ constexpr int kS2WsThreads = kS2Threads + 128;
 constexpr int kS2WsConsumerRegs = 216, kS2WsProducerRegs = 72;
 constexpr int kS2Rows = 16;
 constexpr int kS2Gram = 1, kS2Update = 2, kS2Fused = 3;
+constexpr int kS2InterleaveMaxMT = 12;  // S2Args::interleave is honoured up to this many column tiles
 
 struct S2Args {
   const double* Q; int64_t ldq;
@@ -70,7 +92,6 @@ struct S2Args {
   int nslot;
   int interleave;                   // fused: refill copies interleaved with the G phase (else after it)
   int pf_rounds;                    // L2 prefetch distance in rounds of 8 units (0: off)
-  int issue_loop;                   // copies issued by a loop over the lane's columns (else unrolled)
   int ws;                           // warp-specialised launch (k_stream2<..., true>, kS2WsThreads)
 };
 
@@ -151,7 +172,7 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
     const uint32_t dst = sm0 + 8u * (uint32_t)(sl * SLOT);
     const int64_t row = unit_row(i);
     const int bytes = row_bytes(row);
-    if (a.issue_loop) {
+    if constexpr (PQR_S2_LOOP != 0) {
       double* d = sm + (size_t)sl * SLOT + dsto;
       const double* src = a.Q + (int64_t)cp_jl * a.ldq + row;
       int t = 0;
@@ -239,7 +260,7 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
     // L2 prefetch: round r = units 8r..8r+7 of this CTA (128 contiguous rows); warp (r % 8)
     // prefetches round r + pf_rounds when it starts its unit of round r (one bulk L2 prefetch of
     // the round's rows per column, spread over the lanes): the slot copies then hit L2
-    const int pfr = a.pf_rounds;
+    const int pfr = PQR_S2_PF != 0 ? a.pf_rounds : 0;
     if (pfr > 0) {
       // rounds 0..pfr-1 up front: warp w takes round w (if < pfr)
       for (int r = warp; r < pfr; r += kS2Consumers) {
@@ -332,7 +353,10 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
       }
       // fused pass: the refill of this slot with unit i + NSL is interleaved with the G phase,
       // tile by tile, each tile's copies behind the MMAs that consumed its last reads
-      const bool refill = !WS && MODE == kS2Fused && a.interleave && i + NSL < nu;
+      // (compile-time off past 12 tiles, where it is slower: the skipped copy blocks would
+      // otherwise leave a taken branch per tile group in the MMA stream — instruction-fetch stalls)
+      constexpr bool IL_OK = !WS && MODE == kS2Fused && (MT <= kS2InterleaveMaxMT || PQR_S2_GBAR == 2);
+      const bool refill = IL_OK && a.interleave && i + NSL < nu;
       const uint32_t rdst = sm0 + 8u * (uint32_t)(sl * SLOT);
       const int64_t rrow = unit_row(i + NSL);
       const int rbytes = row_bytes(rrow);
@@ -363,7 +387,9 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
           for (int tg = 0; tg < TG; ++tg) {
             const int mt = m0 + tg;
             if (mt >= MT) break;
-            if (MODE != kS2Fused || 8 * mt + 8 <= k) {
+            // tiles below MT - NT - 1 are Q columns for every k (k >= 8 (MT - 1 - NT) + 1): no
+            // run-time test, so the unrolled tile loop keeps no branch over the shuffle path
+            if (MODE != kS2Fused || (PQR_S2_KTEST == 0 && mt < MT - NT - 1) || 8 * mt + 8 <= k) {
               const double2 a0 = lds2(slot + offG0 + mt * 128), a1 = lds2(slot + offG1 + mt * 128);
               av[tg][0] = a0.x; av[tg][1] = a0.y; av[tg][2] = a1.x; av[tg][3] = a1.y;
             } else {
@@ -392,10 +418,13 @@ __global__ void __launch_bounds__(WS ? kS2WsThreads : kS2Threads, 1) k_stream2(S
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt)
                 if (m0 + tg < MT) dmma884(acc[m0 + tg][nt][0], acc[m0 + tg][nt][1], av[tg][e], bq[nt][e]);
-          if (refill) {
+          if constexpr (!IL_OK && PQR_S2_GBAR == 1) asm volatile("" ::: "memory");
+          if constexpr (IL_OK) {
+            if (refill) {
 #pragma unroll
-            for (int t = 2 * m0; t < 2 * (m0 + TG); ++t)
-              if (t < 2 * MT) copy_t(rdst, rrow, rbytes, t);
+              for (int t = 2 * m0; t < 2 * (m0 + TG); ++t)
+                if (t < 2 * MT) copy_t(rdst, rrow, rbytes, t);
+            }
           }
         }
       }
